@@ -1,0 +1,47 @@
+// Internal declarations shared by the host side (amsim_host.cpp) and the
+// kernel side (amsim_kernels.cu) of libamsim.  Not part of the ABI.
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/amsim.h"
+
+namespace amsim {
+
+constexpr int kMaxDevices = 64;
+
+// Device copy of a table in the kernels' layout: row k (first operand) is
+// 2^m consecutive entries; 16-bit entries hold bits 23..8 of the Alg. 1 entry
+// (carry | top 15 mantissa bits) when every entry's low 8 bits are zero.
+struct DeviceTable {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace amsim
+
+struct amsim_lut {
+    int m = 0;
+    std::vector<uint32_t> entries;   // Alg. 1 layout: (carry << 23) | mantissa
+    int device_entry_bits = 32;      // 16 if every entry has (e & 0xFF) == 0
+    std::mutex mu;
+    amsim::DeviceTable dev[amsim::kMaxDevices];
+};
+
+namespace amsim {
+
+amsim_status set_error(amsim_status s, const std::string &msg);
+void clear_error();
+
+// Device table for the current device (uploads on first use).
+amsim_status device_table(const amsim_lut *lut, const void **ptr, int *entry_bits);
+
+// Global launch counter (incremented by every kernel launch).
+void count_launch(uint64_t n = 1);
+
+int path_policy();
+
+}  // namespace amsim

@@ -1,0 +1,369 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (north_star):
+  * per product: bit-exact (K = 1 outer products, C = +0 + p),
+  * GEMM / conv outputs: |gpu - c64| <= 1e-5 * sum|p| + FLT_MIN per element,
+  * non-split kernels accumulate each output in increasing k from +0 exactly
+    as the oracle's c32, so they are also checked bit-for-bit against c32.
+"""
+import numpy as np
+import pytest
+
+import amsim_inputs as inp
+
+pytestmark = pytest.mark.gpu
+
+FLT_MIN = np.finfo(np.float32).tiny
+
+
+@pytest.fixture(scope="module")
+def am():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback)"
+    from paper_2209_04161_b200 import build
+    build.build()
+    import paper_2209_04161_b200 as am
+    am.amsim_set_path_policy(0)
+    return am
+
+
+@pytest.fixture(scope="module")
+def luts(am):
+    cache = {}
+
+    def get(model, m=7):
+        if (model, m) not in cache:
+            cache[(model, m)] = am.Lut.build(model, m)
+        return cache[(model, m)]
+    return get
+
+
+def dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def host(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def assert_bits(got, want, what=""):
+    g = np.ascontiguousarray(got, np.float32).view(np.uint32)
+    w = np.ascontiguousarray(want, np.float32).view(np.uint32)
+    bad = np.flatnonzero(g.ravel() != w.ravel())
+    assert bad.size == 0, (f"{what}: {bad.size} of {g.size} differ; first at {bad[:5]}: "
+                           f"got {g.ravel()[bad[:5]]} want {w.ravel()[bad[:5]]}")
+
+
+def assert_tol(got, res, what=""):
+    err = np.abs(got.astype(np.float64) - res.c64)
+    tol = 1e-5 * res.abs64 + FLT_MIN
+    bad = np.flatnonzero((err > tol).ravel())
+    assert bad.size == 0, f"{what}: {bad.size} outside tolerance, worst ratio {np.max(err / tol):.3g}"
+
+
+def run_gemm(am, lut, A, B, trans_a=False, trans_b=False, C0=None, accumulate=False):
+    import torch
+    M = A.shape[1] if trans_a else A.shape[0]
+    N = B.shape[0] if trans_b else B.shape[1]
+    C = dev(C0) if C0 is not None else torch.full((M, N), float("nan"), device="cuda")
+    am.amsim_gemm(lut, dev(A), dev(B), C, trans_a, trans_b, accumulate)
+    return host(C)
+
+
+# ---------------------------------------------------------------------------
+# per-product bit-exactness
+
+@pytest.mark.parametrize("model,m", [("exact", 7), ("mitchell", 7), ("mbm", 7), ("exact", 1), ("exact", 4),
+                                     ("exact", 5), ("exact", 6), ("mitchell", 8), ("mitchell", 3)])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_k1_outer_product_exhaustive(am, luts, orc, model, m, policy):
+    """All m-bit mantissas x exponents {1,2,63,64,65,126,127,128,190,253,254}
+    x signs, plus zero/subnormal/Inf/NaN, as a K = 1 outer product
+    (SURVEY.md 8(d) config 1), under automatic and forced-careful dispatch."""
+    v = inp.operand_grid(m)
+    am.amsim_set_path_policy(policy)
+    try:
+        got = run_gemm(am, luts(model, m), v[:, None], v[None, :])
+    finally:
+        am.amsim_set_path_policy(0)
+    want = orc.mul(v[:, None], v[None, :], model, m)
+    assert_bits(got, want, f"{model} m={m} policy={policy}")
+
+
+@pytest.mark.parametrize("model", ["exact", "mitchell", "mbm"])
+def test_fast_path_full_exponent_range(am, luts, orc, model):
+    """Operands whose exponent ranges keep every Exp in [1, 253] take the FTZ
+    fast path; it must equal Alg. 2 bit-for-bit, including Exp = 1 and 253."""
+    g = inp.rng(21)
+    n = 512
+    ea = g.integers(64, 191, n).astype(np.uint32)
+    ea[:2] = (64, 190)
+    a = ((g.integers(0, 2, n).astype(np.uint32) << 31) | (ea << 23) |
+         g.integers(0, 1 << 23, n).astype(np.uint32)).view(np.float32)
+    b = np.roll(a, 3)
+    got = run_gemm(am, luts(model), a[:, None], b[None, :])
+    assert_bits(got, orc.mul(a[:, None], b[None, :], model, 7), model)
+
+
+# ---------------------------------------------------------------------------
+# GEMM
+
+GEMM_SHAPES = [(1, 1, 1), (3, 5, 7), (64, 128, 16), (130, 200, 77), (257, 33, 300), (100, 64, 1000),
+               (65, 129, 17), (5, 300, 31)]
+
+
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+@pytest.mark.parametrize("trans", [(False, False), (True, False), (False, True), (True, True)])
+def test_gemm_vs_oracle(am, luts, orc, shape, trans):
+    M, N, K = shape
+    ta, tb = trans
+    A = inp.normal((M, K), 31)
+    B = inp.normal((K, N), 32)
+    res = orc.gemm(A, B, "mitchell", 7)
+    got = run_gemm(am, luts("mitchell"), A.T.copy() if ta else A, B.T.copy() if tb else B, ta, tb)
+    assert_tol(got, res, f"{shape} {trans}")
+    assert_bits(got, res.c32, f"{shape} {trans} vs c32")
+
+
+def test_gemm_config1_256(am, luts, orc):
+    """BASELINE config 1: 256^3, Mitchell m = 7."""
+    A = inp.normal((256, 256), 1)
+    B = inp.normal((256, 256), 2)
+    res = orc.gemm(A, B, "mitchell", 7)
+    got = run_gemm(am, luts("mitchell"), A, B)
+    assert_bits(got, res.c32)
+    assert_tol(got, res)
+
+
+def test_gemm_leading_dims_and_accumulate(am, luts, orc):
+    import torch
+    M, N, K = 70, 90, 40
+    Abig = inp.normal((M, K + 9), 41)
+    Bbig = inp.normal((K, N + 5), 42)
+    A = dev(Abig)[:, :K]
+    B = dev(Bbig)[:, :N]
+    C0 = inp.normal((M, N + 3), 43)
+    C = dev(C0)
+    lut = luts("exact")
+    am.amsim_gemm(lut, A, B, C[:, :N], accumulate=True)
+    res = orc.gemm(Abig[:, :K], Bbig[:, :N], "exact", 7)
+    got = host(C)
+    want = (C0[:, :N] + res.c32).astype(np.float32)      # C + S, S formed from +0 (header semantics)
+    assert_bits(got[:, :N], want)
+    assert_bits(got[:, N:], C0[:, N:], "columns beyond N untouched")
+
+
+def test_gemm_degenerate(am, luts):
+    import torch
+    lut = luts("exact")
+    C = torch.full((3, 4), 7.0, device="cuda")
+    am.amsim_gemm(lut, torch.empty((3, 0), device="cuda"), torch.empty((0, 4), device="cuda"), C)
+    assert np.all(host(C) == 0.0) and not np.signbit(host(C)).any()
+    C.fill_(7.0)
+    am.amsim_gemm(lut, torch.empty((3, 0), device="cuda"), torch.empty((0, 4), device="cuda"), C, accumulate=True)
+    assert np.all(host(C) == 7.0)
+    am.amsim_gemm(lut, torch.empty((0, 5), device="cuda"), torch.ones((5, 4), device="cuda"),
+                  torch.empty((0, 4), device="cuda"))
+    assert am.lib().amsim_gemm(lut.handle, 0, 0, -1, 2, 2, None, 2, None, 2, None, 2, 0, None) == 1
+
+
+def test_policy_careful_equals_fast(am, luts):
+    A = inp.normal((200, 150), 51)
+    B = inp.normal((150, 170), 52)
+    lut = luts("mitchell")
+    fast = run_gemm(am, lut, A, B)
+    am.amsim_set_path_policy(1)
+    try:
+        careful = run_gemm(am, lut, A, B)
+    finally:
+        am.amsim_set_path_policy(0)
+    assert_bits(fast, careful)
+
+
+def test_determinism(am, luts):
+    A = inp.normal((300, 257), 61)
+    B = inp.normal((257, 190), 62)
+    lut = luts("mbm")
+    assert_bits(run_gemm(am, lut, A, B), run_gemm(am, lut, A, B))
+
+
+def test_dense_layer_passes(am, luts, orc):
+    """AMDENSE as GEMMs with the conv operand order
+    (reading C11): fwd Y = X W (a = x), wgrad dW = X^T dY (a = x),
+    dgrad dX = dY W^T (a = dy).  Asymmetric-order check with the MBM table."""
+    B_, IN, OUT = 64, 400, 120
+    X = inp.relu_normal((B_, IN), 71)
+    W = inp.he_uniform((IN, OUT), IN, 72)
+    dY = inp.normal((B_, OUT), 73, 2 ** -4)
+    lut = luts("mbm")
+    y = run_gemm(am, lut, X, W)
+    dW = run_gemm(am, lut, X, dY, trans_a=True)
+    dX = run_gemm(am, lut, dY, W, trans_b=True)
+    assert_bits(y, orc.gemm(X, W, "mbm").c32)
+    assert_bits(dW, orc.gemm(X.T.copy(), dY, "mbm").c32)
+    assert_bits(dX, orc.gemm(dY, W.T.copy(), "mbm").c32)
+
+
+# ---------------------------------------------------------------------------
+# convolutions
+
+CONV = [
+    # N, H, W, C, K, R, S, stride, pad
+    (2, 5, 5, 3, 4, 3, 3, 1, 0),
+    (2, 7, 6, 3, 2, 3, 3, 2, 1),
+    (1, 8, 8, 2, 3, 3, 3, 3, 1),
+    (2, 6, 6, 4, 5, 1, 1, 2, 0),
+    (1, 9, 7, 2, 2, 5, 5, 2, 2),
+    (3, 4, 4, 1, 1, 2, 2, 1, 0),
+    (2, 12, 12, 8, 36, 3, 3, 1, 1),      # vectorised loads, several N tiles
+    (2, 14, 14, 16, 72, 3, 3, 2, 1),     # stride-2 3x3, C % 4 == 0
+    (3, 9, 9, 12, 130, 1, 1, 2, 0),      # 1x1 stride-2 downsample
+    (2, 20, 20, 3, 16, 7, 7, 2, 3),      # stem geometry
+    (4, 28, 28, 1, 6, 5, 5, 1, 2),       # LeNet c1
+]
+
+
+def _conv_tensors(shape, seed):
+    N, H, W, C, K, R, S, st, pd = shape
+    OH = (H + 2 * pd - R) // st + 1
+    OW = (W + 2 * pd - S) // st + 1
+    x = inp.relu_normal((N, H, W, C), seed)
+    w = inp.he_normal((R, S, C, K), R * S * C, seed + 1)
+    dy = inp.normal((N, OH, OW, K), seed + 2, 0.5)
+    return x, w, dy, OH, OW
+
+
+def _run_conv(am, lut, d, x, w, dy, which):
+    import torch
+    N, H, W, C, K = d.N, d.H, d.W, d.C, d.K
+    if which == "fwd":
+        y = torch.full((N, d.OH, d.OW, K), float("nan"), device="cuda")
+        am.amsim_conv2d_fwd(lut, d, dev(x), dev(w), y)
+        return host(y).reshape(-1, K)
+    if which == "dgrad":
+        dx = torch.full((N, H, W, C), float("nan"), device="cuda")
+        am.amsim_conv2d_bwd_data(lut, d, dev(dy), dev(w), dx)
+        return host(dx).reshape(-1, C)
+    dw = torch.full((d.R, d.S, C, K), float("nan"), device="cuda")
+    nbytes = am.amsim_conv2d_bwd_filter_workspace(lut, d)
+    ws = torch.empty(max(nbytes // 4, 1), device="cuda")
+    am.amsim_conv2d_bwd_filter(lut, d, dev(x), dev(dy), dw, ws)
+    return host(dw).reshape(-1, K)
+
+
+@pytest.mark.parametrize("shape", CONV)
+@pytest.mark.parametrize("which", ["fwd", "dgrad", "wgrad"])
+@pytest.mark.parametrize("model", ["mitchell", "exact"])
+def test_conv_vs_oracle(am, luts, orc, shape, which, model):
+    N, H, W, C, K, R, S, st, pd = shape
+    x, w, dy, OH, OW = _conv_tensors(shape, 100)
+    d = am.conv_desc(N, H, W, C, K, R, S, st, pd)
+    od = orc.conv_desc(N, H, W, C, K, R, S, st, pd)
+    omodel = model
+    lut = luts(omodel)
+    got = _run_conv(am, lut, d, x, w, dy, which)
+    if which == "fwd":
+        res = orc.conv_fwd(od, x, w, omodel)
+    elif which == "dgrad":
+        res = orc.conv_bwd_data(od, dy, w, omodel)
+    else:
+        res = orc.conv_bwd_filter(od, x, dy, omodel)
+    assert_tol(got, res, f"{which} {shape}")
+    if which != "wgrad" or am.amsim_conv2d_bwd_filter_workspace(lut, d) == 0:
+        assert_bits(got, res.c32, f"{which} {shape} vs c32")
+
+
+def test_conv_operand_order_asymmetric(am, orc):
+    """An asymmetric table must give a = x for fwd/wgrad and a = dy for dgrad
+    (reading C11).  The user model is a Python callback passed through the
+    function-pointer ABI: exact product of a with b's significand cut to 3
+    fraction bits (the oracle implements the same model independently in C)."""
+    import struct
+    from paper_2209_04161_b200 import _lib
+
+    @_lib.MUL_FN
+    def asym(a, b):
+        ub = struct.unpack("<I", struct.pack("<f", b))[0] & 0xFFF00000
+        return a * struct.unpack("<f", struct.pack("<I", ub))[0]
+
+    lut = am.Lut.build(asym, 7)
+    shape = (2, 9, 9, 4, 8, 3, 3, 2, 1)
+    N, H, W, C, K, R, S, st, pd = shape
+    x, w, dy, OH, OW = _conv_tensors(shape, 200)
+    d = am.conv_desc(N, H, W, C, K, R, S, st, pd)
+    od = orc.conv_desc(N, H, W, C, K, R, S, st, pd)
+    for which, res in (("fwd", orc.conv_fwd(od, x, w, "asym")), ("dgrad", orc.conv_bwd_data(od, dy, w, "asym")),
+                       ("wgrad", orc.conv_bwd_filter(od, x, dy, "asym"))):
+        got = _run_conv(am, lut, d, x, w, dy, which)
+        assert_bits(got, res.c32, which)
+
+
+@pytest.mark.parametrize("model", ["mbm", "exact"])
+def test_lenet5_step_layers(am, luts, orc, model):
+    """BASELINE config 2 shapes (LeNet-5, batch 64) with MNIST-like inputs."""
+    lut = luts(model)
+    for i, L in enumerate(inp.lenet5_layers(64)):
+        if isinstance(L, inp.ConvLayer):
+            shape = (L.N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad)
+            x = inp.mnist_like((L.N, L.H, L.W, L.C), 3 + i) if L.first else inp.relu_normal((L.N, L.H, L.W, L.C), 3 + i)
+            w = inp.he_uniform((L.R, L.S, L.C, L.K), L.R * L.S * L.C, 4 + i)
+            dy = inp.normal((L.N, L.OH, L.OW, L.K), 5 + i, 2 ** -8)
+            d = am.conv_desc(*shape)
+            od = orc.conv_desc(*shape)
+            assert_bits(_run_conv(am, lut, d, x, w, dy, "fwd"), orc.conv_fwd(od, x, w, model).c32, L.name)
+            r = orc.conv_bwd_filter(od, x, dy, model)
+            assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), r, L.name)
+            if not L.first:
+                assert_bits(_run_conv(am, lut, d, x, w, dy, "dgrad"), orc.conv_bwd_data(od, dy, w, model).c32, L.name)
+        else:
+            X = inp.relu_normal((L.N, L.IN), 3 + i)
+            W = inp.he_uniform((L.IN, L.OUT), L.IN, 4 + i)
+            dY = inp.normal((L.N, L.OUT), 5 + i, 2 ** -8)
+            assert_bits(run_gemm(am, lut, X, W), orc.gemm(X, W, model).c32, L.name)
+            assert_bits(run_gemm(am, lut, X, dY, trans_a=True), orc.gemm(X.T.copy(), dY, model).c32, L.name)
+            assert_bits(run_gemm(am, lut, dY, W, trans_b=True), orc.gemm(dY, W.T.copy(), model).c32, L.name)
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE sizes, sampled outputs
+
+FULL_LAYERS = ["stem", "l1.0.conv2", "l2.0.conv2", "l2.0.down", "l4.0.conv2", "l4.2.conv3"]
+
+
+@pytest.mark.parametrize("name", FULL_LAYERS)
+def test_resnet50_full_size_sampled(am, luts, orc, name):
+    """ResNet-50 b256 layers at full size in the bench's launch configuration;
+    the oracle recomputes sampled output rows one by one."""
+    import torch
+    L = {l.name: l for l in inp.resnet50_layers(256)}[name]
+    shape = (L.N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad)
+    d = am.conv_desc(*shape)
+    od = orc.conv_desc(*shape)
+    g = inp.rng(7)
+    x = inp.relu_normal((L.N, L.H, L.W, L.C), 1000)
+    w = inp.he_normal((L.R, L.S, L.C, L.K), L.R * L.S * L.C, 1001)
+    dy = inp.normal((L.N, L.OH, L.OW, L.K), 1002, 2 ** -10)
+    lut = luts("exact")
+    y = _run_conv(am, lut, d, x, w, dy, "fwd")
+    rows = np.unique(np.concatenate([[0, y.shape[0] - 1], g.integers(0, y.shape[0], 14)]))
+    res = orc.conv_fwd(od, x, w, "exact", rows=rows)
+    assert_bits(y[rows], res.c32, f"{name} fwd")
+    if not L.first:
+        dx = _run_conv(am, lut, d, x, w, dy, "dgrad")
+        rows = np.unique(np.concatenate([[0, dx.shape[0] - 1], g.integers(0, dx.shape[0], 14)]))
+        res = orc.conv_bwd_data(od, dy, w, "exact", rows=rows)
+        assert_bits(dx[rows], res.c32, f"{name} dgrad")
+    dw = _run_conv(am, lut, d, x, w, dy, "wgrad")
+    rows = np.unique(np.concatenate([[0, dw.shape[0] - 1], g.integers(0, dw.shape[0], 6)]))
+    res = orc.conv_bwd_filter(od, x, dy, "exact", rows=rows)
+    assert_tol(dw[rows], res, f"{name} wgrad")
+    torch.cuda.empty_cache()
+
+
+def test_lut_lookup_microbench(am):
+    idx = inp.rng(3).integers(0, 128, 1 << 16).astype(np.uint32)
+    r = am.amsim_bench_lut_lookup(7, 16, idx, iters=256)
+    assert r > 1e11
