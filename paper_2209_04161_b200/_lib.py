@@ -200,11 +200,13 @@ def amsim_gemm(lut: Lut, A, B, C, trans_a: bool = False, trans_b: bool = False, 
     M = A.shape[1] if trans_a else A.shape[0]
     K = A.shape[0] if trans_a else A.shape[1]
     N = B.shape[0] if trans_b else B.shape[1]
+    lds = []
     for t, nm in ((A, "A"), (B, "B"), (C, "C")):
-        if t.dim() != 2 or t.stride(1) != 1:
+        if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
             raise ValueError(f"{nm} must be 2-D with unit column stride")
-    _check(lib().amsim_gemm(lut.handle, int(trans_a), int(trans_b), M, N, K, _dptr(A, "A"), A.stride(0),
-                            _dptr(B, "B"), B.stride(0), _dptr(C, "C"), C.stride(0), int(accumulate),
+        lds.append(t.stride(0) if t.shape[0] > 1 else t.shape[1])  # a size-1 dim's stride is arbitrary
+    _check(lib().amsim_gemm(lut.handle, int(trans_a), int(trans_b), M, N, K, _dptr(A, "A"), lds[0],
+                            _dptr(B, "B"), lds[1], _dptr(C, "C"), lds[2], int(accumulate),
                             _stream(stream)), "amsim_gemm")
     return C
 

@@ -578,21 +578,22 @@ __global__ void __launch_bounds__(NT, 1) lut_bench_kernel(const void *lut, uint3
     __syncthreads();
     constexpr int ebl = EB == 16 ? 1 : 2;
     const uint32_t base = smem_u32(smem);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t bof[4], aof[TM];
-    for (int c = 0; c < 4; c++) bof[c] = bidx[(blockIdx.x * NT + threadIdx.x * 4 + c) % nidx] << ebl;
-    for (int r = 0; r < TM; r++) aof[r] = base + ((((warp * 37 + r * 11 + blockIdx.x) * 13) & ((1u << m) - 1)) << (m + ebl));
+    const int warp = threadIdx.x >> 5;
+    const uint32_t rmask = (1u << m) - 1u;
+    uint32_t bof[4], row[TM];
+    for (int c = 0; c < 4; c++) bof[c] = base + (bidx[(blockIdx.x * NT + threadIdx.x * 4 + c) % nidx] << ebl);
+    for (int r = 0; r < TM; r++) row[r] = ((warp * 37 + r * 11 + blockIdx.x) * 13) & rmask;
     float acc[TM][4] = {};
     for (int it = 0; it < iters; it++) {
 #pragma unroll
-        for (int r = 0; r < TM; r++)
+        for (int r = 0; r < TM; r++) {
+            const uint32_t aof = ((row[r] + uint32_t(it)) & rmask) << (m + ebl);  // warp-uniform row walk
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                uint32_t e = lds_entry<EB>(aof[r] + bof[c]);
+                uint32_t e = lds_entry<EB>(aof + bof[c]);
                 acc[r][c] = fma_ftz(__uint_as_float(e * 256u + 0x3F800000u), 1.0f, acc[r][c]);
             }
-#pragma unroll
-        for (int r = 0; r < TM; r++) aof[r] ^= ((it & 7) + 1) << (m + ebl);  // walk rows (stays in table)
+        }
     }
     float s = 0.f;
     for (int r = 0; r < TM; r++)
