@@ -128,8 +128,9 @@ float amsim_model_mbm(float a, float b);
  * row-major storage; op(A) is M x K (A stored M x K with leading dimension
  * lda, or K x M when trans_a), op(B) is K x N (B stored K x N, ldb, or
  * N x K when trans_b), C is M x N with ldc >= N.  S is formed from +0 in
- * increasing t (split only when K is very large; then the per-split partial
- * sums are added in increasing split order).
+ * increasing t; the tile planner may split t into contiguous chunks to
+ * balance the SMs (partials then added in increasing chunk order, on a
+ * stream-ordered scratch allocation; policy bit 1 disables splitting).
  * M, N or K = 0 is valid (K = 0 sets C to +0, or leaves it with accumulate).
  * Dense layers: fwd Y = X W (a = x, b = w), wgrad dW = X^T dY (trans_a,
  * a = x, b = dy), dgrad dX = dY W^T (trans_b, a = dy, b = w).
@@ -182,10 +183,14 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
 /* ---------------------------------------------------------------------- */
 /* Test and measurement hooks                                               */
 
-/* Product-path policy: 0 = automatic (per smem tile: the FTZ fast path when
- * the tile's exponent ranges make it bit-identical to Alg. 2, else the
- * literal Alg. 2 careful path), 1 = force the careful path everywhere.
- * Process-wide. */
+/* Execution policy (process-wide bit set, default 0):
+ *   bit 0 -- force the literal Alg. 2 careful path everywhere (default: per
+ *            smem tile, the FTZ fast path when the tile's exponent ranges make
+ *            it bit-identical to Alg. 2, else the careful path);
+ *   bit 1 -- never split K: every output is then the FP32 sum from +0 in
+ *            increasing k, bit-identical to a sequential reference (default:
+ *            the tile planner may split K to balance the SMs; partials are
+ *            reduced in a fixed order, so results stay deterministic). */
 amsim_status amsim_set_path_policy(int policy);
 
 /* Kernel launches issued by this library in this process (all entry points). */

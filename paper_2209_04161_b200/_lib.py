@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libamsim.so")
+LIB_PATH = os.environ.get("AMSIM_LIB") or os.path.join(PKG, "libamsim.so")
 
 AMSIM_OK = 0
 _STATUS = {0: "AMSIM_OK", 1: "AMSIM_ERR_INVALID_ARG", 2: "AMSIM_ERR_UNSUPPORTED", 3: "AMSIM_ERR_MODEL",

@@ -21,7 +21,8 @@ SOURCES = [
     ("amsim_host.cpp", "g++"),
     ("amsim_kernels.cu", "nvcc"),
 ]
-HEADERS = [os.path.join(CSRC, "amsim_internal.h"), os.path.join(ROOT, "include", "amsim.h")]
+HEADERS = [os.path.join(CSRC, "amsim_internal.h"), os.path.join(CSRC, "amsim_device.cuh"),
+           os.path.join(ROOT, "include", "amsim.h")]
 
 
 def _newer(target: str, deps) -> bool:
@@ -64,5 +65,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(tag: str, defines) -> str:
+    """Experimental build with extra -D flags (tuning sweeps): build/variants/libamsim_<tag>.so.
+    Load it by setting AMSIM_LIB to the returned path."""
+    vdir = os.path.join(BUILD, "variants")
+    os.makedirs(vdir, exist_ok=True)
+    host_o = os.path.join(BUILD, "amsim_host.cpp.o")
+    build()  # host object
+    ko = os.path.join(vdir, f"kernels_{tag}.o")
+    so = os.path.join(vdir, f"libamsim_{tag}.so")
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+           *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           "-c", os.path.join(CSRC, "amsim_kernels.cu"), "-o", ko]
+    subprocess.run(cmd, check=True)
+    subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", so, host_o, ko, "-lpthread", "-ldl", "-lrt"],
+                   check=True)
+    return so
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,608 @@
+// libamsim device code: the AMSim LUT GEMM core (persistent, one CTA per SM)
+// and its operand address maps for dense GEMM and NHWC conv fwd / bwd-data /
+// bwd-filter (implicit GEMM).  Citations "PAPER.md:L" are lines of
+// /root/reference/PAPER.md; DESIGN.md has the derivation.
+//
+//  * The CTA holds the 2^(2m)-entry mantissa-product table in shared memory
+//    for the whole launch (the paper used texture memory).
+//  * Operand k-tiles are staged into shared memory asynchronously (cp.async
+//    with zero fill for padding / ragged edges; completion tracked by one
+//    mbarrier per stage, STAGES deep) and DECODED ONCE per tile into
+//    (alpha, offset) pairs: alpha = sign|exponent bits = +-2^(e-127) or +-0,
+//    offset = the top-m mantissa bits pre-scaled to a table byte offset
+//    (Alg. 2 l.1-2; reading C1).  The paper decodes inside
+//    AMSim for every product.
+//  * The 32 lanes of a warp share the A element (same table row) and take
+//    32*TN different B columns, so one warp-wide lookup touches a single
+//    2^m-entry row (m = 7, 16-bit entries: 64 words on 32 banks, <= 2
+//    wavefronts).
+//  * Fast path per product: e = LUT[rowoff(a) + off(b)]; x = e*mul_b + alpha_b
+//    (integer add into the exponent field: x = +-(1.mant*2^carry)*2^(eb-127);
+//    mul_b = 0 makes x = +-0 when b is zero); acc = fma.rn.ftz(x, alpha_a, acc).
+//    FTZ realises Alg. 2's Exp <= 0 -> 0.  Taken only for smem tiles whose
+//    exponent ranges make it bit-identical to Alg. 2; otherwise the careful
+//    path evaluates Alg. 2 literally.
+//  * acc starts at +0 and adds products in increasing k (FP32).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace amsim {
+namespace dev {
+
+constexpr int BK = 16;
+constexpr int STAGES = 3;
+constexpr int RAW_PAD = 4;    // row padding of k-contiguous raw tiles (keeps 16-B alignment)
+constexpr int MAX_SUB = 9;    // sub-problems per launch (stride phases of dgrad, S <= 3)
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float *src, bool valid)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0));
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float *src, bool valid)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
+}
+
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ float fma_ftz(float a, float b, float c)
+{
+    float d;
+    asm("fma.rn.ftz.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+__device__ __forceinline__ float add_ftz(float a, float b)
+{
+    float d;
+    asm("add.rn.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+
+template <int EB>
+__device__ __forceinline__ uint32_t lds_entry(uint32_t addr)
+{
+    uint32_t v;
+    if constexpr (EB == 16)
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+    else
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// Unsigned division by a runtime constant (n < 2^31).
+struct FastDiv {
+    uint32_t d, mul, shr;
+    __host__ void init(uint32_t div)
+    {
+        d = div ? div : 1;
+        shr = 0;
+        while ((1ull << shr) < d) shr++;
+        mul = uint32_t(((1ull << 32) * ((1ull << shr) - d)) / d + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const
+    {
+        return uint32_t((uint64_t(__umulhi(n, mul)) + n) >> shr);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Problem description: up to MAX_SUB independent sub-GEMMs sharing N (the
+// stride phases of dgrad), each optionally split along K (wgrad).
+
+struct SubP {
+    int M, K;             // rows and reduction length of this sub-problem
+    int tiles_m, splits, kchunk;
+    int tile_begin;       // first global tile index
+    int64_t ws_offset;    // element offset of this sub's split partials [splits][M][N] in the workspace
+};
+
+struct OpDesc {
+    int kcontig;          // raw tile stored [mn][BK + RAW_PAD] (k contiguous) or [BK][BMN]
+    int vec_log2;         // 0 (4-byte copies) or 2 (16-byte copies along the contiguous dim)
+};
+
+struct KParams {
+    int N, tiles_n, nsub, ntiles;
+    SubP sub[MAX_SUB];
+    float *C;             // output (ldc-strided rows, A map's out_row)
+    float *ws;            // split-K partials (subs with splits > 1)
+    int64_t ws_elems;     // workspace size in floats (0: no split)
+    int cfg;              // host-side tile configuration id
+    int64_t ldc;
+    int accumulate;
+    OpDesc da, db;
+    const void *lut;      // device table (global); copied to shared memory
+    int m_bits;
+    uint32_t lut_bytes;
+    int policy;           // 1 = force the careful path
+};
+
+// ---------------------------------------------------------------------------
+// Operand address maps: at(s, mn, k) -> address of element (mn, k) of
+// sub-problem s (mn = GEMM row for A, column for B) or nullptr for an implicit
+// zero (padding, dilation, ragged edge).  A maps also give the output row
+// offset of GEMM row `row` (out_row).
+
+struct GemmOp {
+    const float *p;
+    int64_t ld;
+    int MN, K;
+    int kcontig;
+    __device__ __forceinline__ const float *at(int, int mn, int k) const
+    {
+        if (mn >= MN || k >= K) return nullptr;
+        return kcontig ? p + int64_t(mn) * ld + k : p + int64_t(k) * ld + mn;
+    }
+    __device__ __forceinline__ int64_t out_row(int, int row, int64_t ldc) const { return int64_t(row) * ldc; }
+};
+
+struct ConvGeom {
+    int N, H, W, C, K, R, S, sh, sw, ph, pw, OH, OW;
+    FastDiv fOHOW, fOW, fSC, fC;
+};
+
+// fwd A: element (m = (n,oh,ow), k = (kh,kw,ci)) of IM2COL(x) (Alg. 3 l.4)
+struct FwdX {
+    const float *x;
+    ConvGeom g;
+    int M, Kd;
+    __device__ __forceinline__ const float *at(int, int m, int k) const
+    {
+        if (m >= M || k >= Kd) return nullptr;
+        uint32_t n = g.fOHOW.div(m), r = m - n * uint32_t(g.OH * g.OW);
+        uint32_t oh = g.fOW.div(r), ow = r - oh * g.OW;
+        uint32_t kh = g.fSC.div(k), r2 = k - kh * uint32_t(g.S * g.C);
+        uint32_t kw = g.fC.div(r2), ci = r2 - kw * g.C;
+        int ih = int(oh) * g.sh - g.ph + int(kh), iw = int(ow) * g.sw - g.pw + int(kw);
+        if (ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) return nullptr;
+        return x + ((int64_t(n) * g.H + ih) * g.W + iw) * g.C + ci;
+    }
+    __device__ __forceinline__ int64_t out_row(int, int row, int64_t ldc) const { return int64_t(row) * ldc; }
+};
+
+// wgrad A: element (mn = (kh,kw,ci), k = (n,oh,ow)) = x[n][oh*s-p+kh][ow*s-p+kw][ci]
+// (IM2COL_Weight with the error's dilation skipped)
+struct WgX {
+    const float *x;
+    ConvGeom g;
+    int M, Kd;
+    __device__ __forceinline__ const float *at(int, int mn, int k) const
+    {
+        if (mn >= M || k >= Kd) return nullptr;
+        uint32_t kh = g.fSC.div(mn), r2 = mn - kh * uint32_t(g.S * g.C);
+        uint32_t kw = g.fC.div(r2), ci = r2 - kw * g.C;
+        uint32_t n = g.fOHOW.div(k), r = k - n * uint32_t(g.OH * g.OW);
+        uint32_t oh = g.fOW.div(r), ow = r - oh * g.OW;
+        int ih = int(oh) * g.sh - g.ph + int(kh), iw = int(ow) * g.sw - g.pw + int(kw);
+        if (ih < 0 || ih >= g.H || iw < 0 || iw >= g.W) return nullptr;
+        return x + ((int64_t(n) * g.H + ih) * g.W + iw) * g.C + ci;
+    }
+    __device__ __forceinline__ int64_t out_row(int, int row, int64_t ldc) const { return int64_t(row) * ldc; }
+};
+
+// dgrad, per stride phase (a, b) in [0,sh) x [0,sw): the output pixels
+// h = sh*u + ch with ch = (a - ph) mod sh receive contributions only from the
+// taps kh = a, a+sh, ... (the other taps of IM2COL_PLG(pad(dilate(dy))) read
+// the dilated zeros, and are skipped exactly, reading C14).
+// Taps run in the paper's order: kh' = R-1-kh increasing (reverse_transpose,
+// PAPER.md:582), then kw', then co.
+struct DgPhase {
+    int a, b, ch, cw;     // phase and first output row / column of the phase
+    int th, tw;           // valid taps per axis
+    int Hp, Wp;           // output rows / columns of the phase
+    FastDiv fHpWp, fWp, fTwK;
+};
+
+struct DgDY {
+    const float *dy;
+    ConvGeom g;
+    DgPhase ph[MAX_SUB];
+    FastDiv fK;
+    __device__ __forceinline__ const float *at(int s, int m, int k) const
+    {
+        const DgPhase &P = ph[s];
+        if (m >= g.N * P.Hp * P.Wp || k >= P.th * P.tw * g.K) return nullptr;
+        uint32_t n = P.fHpWp.div(m), r = m - n * uint32_t(P.Hp * P.Wp);
+        uint32_t u = P.fWp.div(r), v = r - u * P.Wp;
+        uint32_t i = P.fTwK.div(k), r2 = k - i * uint32_t(P.tw * g.K);
+        uint32_t j = fK.div(r2), co = r2 - j * g.K;
+        int kh = P.a + g.sh * (P.th - 1 - int(i)), kw = P.b + g.sw * (P.tw - 1 - int(j));
+        int h = g.sh * int(u) + P.ch, w = g.sw * int(v) + P.cw;
+        int oh = (h + g.ph - kh) / g.sh, ow = (w + g.pw - kw) / g.sw;  // exact by construction
+        if (h + g.ph - kh < 0 || w + g.pw - kw < 0 || oh >= g.OH || ow >= g.OW) return nullptr;
+        return dy + ((int64_t(n) * g.OH + oh) * g.OW + ow) * g.K + co;
+    }
+    __device__ __forceinline__ int64_t out_row(int s, int row, int64_t ldc) const
+    {
+        const DgPhase &P = ph[s];
+        uint32_t n = P.fHpWp.div(row), r = row - n * uint32_t(P.Hp * P.Wp);
+        uint32_t u = P.fWp.div(r), v = r - u * P.Wp;
+        int h = g.sh * int(u) + P.ch, w = g.sw * int(v) + P.cw;
+        return ((int64_t(n) * g.H + h) * g.W + w) * ldc;
+    }
+};
+
+// dgrad B: reverse_transpose(w) restricted to the phase's taps:
+// element (mn = ci, k = (i, j, co)) = w[kh][kw][ci][co]
+struct DgW {
+    const float *w;
+    ConvGeom g;
+    DgPhase ph[MAX_SUB];
+    FastDiv fK;
+    __device__ __forceinline__ const float *at(int s, int ci, int k) const
+    {
+        const DgPhase &P = ph[s];
+        if (ci >= g.C || k >= P.th * P.tw * g.K) return nullptr;
+        uint32_t i = P.fTwK.div(k), r2 = k - i * uint32_t(P.tw * g.K);
+        uint32_t j = fK.div(r2), co = r2 - j * g.K;
+        int kh = P.a + g.sh * (P.th - 1 - int(i)), kw = P.b + g.sw * (P.tw - 1 - int(j));
+        return w + ((int64_t(kh) * g.S + kw) * g.C + ci) * g.K + co;
+    }
+};
+
+// ---------------------------------------------------------------------------
+
+template <int NT_, int TM_, int TN_>
+struct KCfg {
+    static constexpr int NT = NT_;
+    static constexpr int NWARPS = NT / 32;
+    static constexpr int TM = TM_;
+    static constexpr int TN = TN_;
+    static constexpr int BM = NWARPS * TM;
+    static constexpr int BN = 32 * TN;
+    static constexpr int RAW_A = BM * (BK + RAW_PAD);
+    static constexpr int RAW_B = BN * (BK + RAW_PAD);
+    static constexpr int RAW_STAGE = RAW_A + RAW_B;        // floats
+    static constexpr int DEC = 2 * BK * (BM + BN);         // u32 per buffer (alpha + offset)
+    static size_t smem_bytes(uint32_t lut_bytes)
+    {
+        size_t lut = (lut_bytes + 127) & ~size_t(127);
+        return lut + sizeof(float) * RAW_STAGE * STAGES + sizeof(uint32_t) * DEC * 2 + sizeof(uint32_t) * NWARPS * 2 +
+               8 * STAGES + 128;
+    }
+};
+
+template <int NT, int ROWS, class Op>
+__device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, float *raw, int s, int mn0, int k0,
+                                              int kend, const float *dummy)
+{
+    static_assert((ROWS & (ROWS - 1)) == 0, "tile rows must be a power of two");
+    constexpr int ROWS_LOG2 = __builtin_ctz(ROWS);
+    const int tid = threadIdx.x;
+    const int vl = d.vec_log2;
+    if (d.kcontig) {  // raw [ROWS][BK + RAW_PAD]
+        const int cpr_log2 = 4 - vl;  // chunks per row, BK = 16
+        const int total = ROWS << cpr_log2;
+        for (int c = tid; c < total; c += NT) {
+            int i = c >> cpr_log2, kk = (c & ((1 << cpr_log2) - 1)) << vl;
+            int k = k0 + kk;
+            const float *src = (k < kend) ? op.at(s, mn0 + i, k) : nullptr;
+            uint32_t dst = smem_u32(raw + i * (BK + RAW_PAD) + kk);
+            if (vl == 2)
+                cp_async16(dst, src ? src : dummy, src != nullptr);
+            else
+                cp_async4(dst, src ? src : dummy, src != nullptr);
+        }
+    } else {  // raw [BK][ROWS]
+        const int cpr_log2 = ROWS_LOG2 - vl;
+        const int total = BK << cpr_log2;
+        for (int c = tid; c < total; c += NT) {
+            int kk = c >> cpr_log2, i = (c & ((1 << cpr_log2) - 1)) << vl;
+            int k = k0 + kk;
+            const float *src = (k < kend) ? op.at(s, mn0 + i, k) : nullptr;
+            uint32_t dst = smem_u32(raw + kk * ROWS + i);
+            if (vl == 2)
+                cp_async16(dst, src ? src : dummy, src != nullptr);
+            else
+                cp_async4(dst, src ? src : dummy, src != nullptr);
+        }
+    }
+}
+
+// Decode one raw operand tile into (alpha, offset) arrays laid out [BK][rows];
+// tracks min / max exponent fields over nonzero elements.
+template <int NT, int ROWS>
+__device__ __forceinline__ void decode_operand(const float *raw, int kcontig, uint32_t *al, uint32_t *off, int shift,
+                                               uint32_t mask, int off_shift, uint32_t off_base, uint32_t &emin,
+                                               uint32_t &emax)
+{
+    constexpr int total = BK * ROWS;
+#pragma unroll
+    for (int e0 = 0; e0 < total; e0 += NT) {
+        const int e = e0 + threadIdx.x;
+        if (total % NT == 0 || e < total) {
+            const int kk = e / ROWS, i = e % ROWS;
+            float v = kcontig ? raw[i * (BK + RAW_PAD) + kk] : raw[kk * ROWS + i];
+            uint32_t u = __float_as_uint(v);
+            uint32_t ex = (u >> 23) & 0xFFu;
+            al[e] = u & 0xFF800000u;
+            off[e] = off_base + (((u >> shift) & mask) << off_shift);
+            if (ex) {
+                emin = min(emin, ex);
+                emax = max(emax, ex);
+            }
+        }
+    }
+}
+
+template <class Cf, int EB, class OpA, class OpB>
+__global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_constant__ KParams p,
+                                                             const __grid_constant__ OpA opa,
+                                                             const __grid_constant__ OpB opb)
+{
+    constexpr int NT = Cf::NT, NWARPS = Cf::NWARPS, TM = Cf::TM, TN = Cf::TN, BM = Cf::BM, BN = Cf::BN;
+    extern __shared__ __align__(128) unsigned char smem[];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lut_pad = (p.lut_bytes + 127u) & ~127u;
+    unsigned char *lut_s = smem;
+    float *raw = reinterpret_cast<float *>(smem + lut_pad);
+    uint32_t *dec = reinterpret_cast<uint32_t *>(raw + Cf::RAW_STAGE * STAGES);
+    uint32_t *wflags = dec + Cf::DEC * 2;  // [2][NWARPS]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(wflags + NWARPS * 2);
+
+    // table -> shared memory, once per persistent CTA
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.lut);
+        uint4 *dst = reinterpret_cast<uint4 *>(lut_s);
+        for (uint32_t i = tid; i < p.lut_bytes / 16; i += NT) dst[i] = src[i];
+        for (uint32_t i = (p.lut_bytes / 16) * 16 + tid; i < p.lut_bytes; i += NT)
+            lut_s[i] = reinterpret_cast<const unsigned char *>(p.lut)[i];
+    }
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) mbar_init(smem_u32(&bars[s]), NT);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    const int m = p.m_bits;
+    const int shift = 23 - m;
+    const uint32_t mask = (1u << m) - 1u;
+    constexpr int ebytes_log2 = EB == 16 ? 1 : 2;
+    const uint32_t lut_base = smem_u32(lut_s);
+    constexpr uint32_t MULV = EB == 16 ? 256u : 1u;
+    const float *dummy = reinterpret_cast<const float *>(p.lut);  // valid global address for 0-byte copies
+
+    struct Tile {
+        int s, m0, n0, kb, ke, split;
+    };
+    auto tile_of = [&](int t) {
+        Tile T;
+        int s = 0;
+        while (s + 1 < p.nsub && t >= p.sub[s + 1].tile_begin) s++;
+        const SubP &S = p.sub[s];
+        int local = t - S.tile_begin;
+        int tn = local % p.tiles_n;
+        int r = local / p.tiles_n;
+        int tm = r % S.tiles_m;
+        T.split = r / S.tiles_m;
+        T.s = s;
+        T.m0 = tm * BM;
+        T.n0 = tn * BN;
+        T.kb = T.split * S.kchunk;
+        T.ke = min(S.K, T.kb + S.kchunk);
+        return T;
+    };
+    auto ktiles_of = [&](const Tile &T) { return T.ke > T.kb ? (T.ke - T.kb + BK - 1) / BK : 0; };
+
+    // issue cursor (runs STAGES-1 k-tiles ahead of the compute cursor)
+    int itile = blockIdx.x, ik = 0, ig = 0;
+    Tile IT;
+    if (itile < p.ntiles) IT = tile_of(itile);
+    auto issue_next = [&]() {
+        while (itile < p.ntiles) {
+            int kt = ktiles_of(IT);
+            if (ik >= kt) {  // empty k range
+                itile += gridDim.x;
+                ik = 0;
+                if (itile < p.ntiles) IT = tile_of(itile);
+                continue;
+            }
+            int stage = ig % STAGES;
+            float *ra = raw + stage * Cf::RAW_STAGE;
+            float *rb = ra + Cf::RAW_A;
+            int k0 = IT.kb + ik * BK;
+            issue_operand<NT, BM>(opa, p.da, ra, IT.s, IT.m0, k0, IT.ke, dummy);
+            issue_operand<NT, BN>(opb, p.db, rb, IT.s, IT.n0, k0, IT.ke, dummy);
+            cp_async_arrive_noinc(smem_u32(&bars[stage]));
+            ig++;
+            if (++ik == kt) {
+                ik = 0;
+                itile += gridDim.x;
+                if (itile < p.ntiles) IT = tile_of(itile);
+            }
+            return;
+        }
+    };
+    for (int s = 0; s < STAGES - 1; s++) issue_next();
+
+    float acc[TM][TN];
+    int g = 0;
+    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        const Tile T = tile_of(tile);
+        const int KT = ktiles_of(T);
+#pragma unroll
+        for (int r = 0; r < TM; r++)
+#pragma unroll
+            for (int c = 0; c < TN; c++) acc[r][c] = 0.0f;
+
+        for (int kt = 0; kt < KT; kt++, g++) {
+            issue_next();
+            const int stage = g % STAGES;
+            mbar_wait(smem_u32(&bars[stage]), uint32_t((g / STAGES) & 1));
+            const float *ra = raw + stage * Cf::RAW_STAGE;
+            const float *rb = ra + Cf::RAW_A;
+            uint32_t *d = dec + (g & 1) * Cf::DEC;
+            uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + 2 * BK * BM, *b_off = b_al + BK * BN;
+            uint32_t amin = 255, amax = 0, bmin = 255, bmax = 0;
+            decode_operand<NT, BM>(ra, p.da.kcontig, a_al, a_off, shift, mask, m + ebytes_log2, lut_base, amin, amax);
+            decode_operand<NT, BN>(rb, p.db.kcontig, b_al, b_off, shift, mask, ebytes_log2, 0u, bmin, bmax);
+            amin = __reduce_min_sync(0xffffffffu, amin);
+            amax = __reduce_max_sync(0xffffffffu, amax);
+            bmin = __reduce_min_sync(0xffffffffu, bmin);
+            bmax = __reduce_max_sync(0xffffffffu, bmax);
+            uint32_t *wf = wflags + (g & 1) * NWARPS;
+            if (lane == 0) wf[warp] = amin | (amax << 8) | (bmin << 16) | (bmax << 24);
+            __syncthreads();
+
+            uint32_t lo = 0xFFFFFFFFu, hi = 0u;  // byte-wise mins (bytes 0, 2), maxs (bytes 1, 3)
+#pragma unroll
+            for (int w = 0; w < NWARPS; w++) {
+                uint32_t v = wf[w];
+                lo = __vminu4(lo, v | 0xFF00FF00u);
+                hi = __vmaxu4(hi, v & 0xFF00FF00u);
+            }
+            const int Amin = lo & 0xFF, Bmin = (lo >> 16) & 0xFF, Amax = (hi >> 8) & 0xFF, Bmax = hi >> 24;
+            // The fast path equals Alg. 2 bit-for-bit when alpha_a is finite
+            // (ea <= 254), x = entry * 2^(eb-127) is finite (eb <= 253) and,
+            // for every pair of nonzero operands, 1 <= Exp (ea + eb >= 128)
+            // and Exp + carry <= 254 (ea + eb <= 380).  Min / max run over the
+            // nonzero elements of the two smem tiles (conservative).
+            const bool fast = p.policy == 0 && Amax <= 254 && Bmax <= 253 &&
+                              (Amax == 0 || Bmax == 0 || (Amin + Bmin >= 128 && Amax + Bmax <= 380));
+
+            const uint32_t *A_al = a_al + warp * TM, *A_off = a_off + warp * TM;
+            const uint32_t *B_al = b_al + lane * TN, *B_off = b_off + lane * TN;
+            if (fast) {
+#pragma unroll 2
+                for (int kk = 0; kk < BK; kk++) {
+                    uint32_t aal[TM], aof[TM], bal[TN], bof[TN], mul[TN];
+#pragma unroll
+                    for (int r = 0; r < TM; r += 4) {
+                        uint4 v = *reinterpret_cast<const uint4 *>(A_al + kk * BM + r);
+                        uint4 o = *reinterpret_cast<const uint4 *>(A_off + kk * BM + r);
+                        aal[r] = v.x; aal[r + 1] = v.y; aal[r + 2] = v.z; aal[r + 3] = v.w;
+                        aof[r] = o.x; aof[r + 1] = o.y; aof[r + 2] = o.z; aof[r + 3] = o.w;
+                    }
+                    if constexpr (TN == 4) {
+                        uint4 v = *reinterpret_cast<const uint4 *>(B_al + kk * BN);
+                        uint4 o = *reinterpret_cast<const uint4 *>(B_off + kk * BN);
+                        bal[0] = v.x; bal[1] = v.y; bal[2] = v.z; bal[3] = v.w;
+                        bof[0] = o.x; bof[1] = o.y; bof[2] = o.z; bof[3] = o.w;
+                    } else if constexpr (TN == 2) {
+                        uint2 v = *reinterpret_cast<const uint2 *>(B_al + kk * BN);
+                        uint2 o = *reinterpret_cast<const uint2 *>(B_off + kk * BN);
+                        bal[0] = v.x; bal[1] = v.y;
+                        bof[0] = o.x; bof[1] = o.y;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < TN; c++) {
+                            bal[c] = B_al[kk * BN + c];
+                            bof[c] = B_off[kk * BN + c];
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < TN; c++) mul[c] = min(bal[c] << 1, MULV);
+#pragma unroll
+                    for (int r = 0; r < TM; r++)
+#pragma unroll
+                        for (int c = 0; c < TN; c++) {
+                            uint32_t e = lds_entry<EB>(aof[r] + bof[c]);
+                            uint32_t x = e * mul[c] + bal[c];
+                            acc[r][c] = fma_ftz(__uint_as_float(x), __uint_as_float(aal[r]), acc[r][c]);
+                        }
+                }
+            } else {
+                // careful path: Alg. 2 literally, readings C4-C7
+                for (int kk = 0; kk < BK; kk++) {
+#pragma unroll
+                    for (int r = 0; r < TM; r++) {
+                        uint32_t aal = A_al[kk * BM + r], aof = A_off[kk * BM + r];
+                        uint32_t ea = (aal >> 23) & 0xFFu;
+#pragma unroll
+                        for (int c = 0; c < TN; c++) {
+                            uint32_t bal = B_al[kk * BN + c], bof = B_off[kk * BN + c];
+                            uint32_t eb = (bal >> 23) & 0xFFu;
+                            uint32_t ent = lds_entry<EB>(aof + bof) * MULV;  // (carry << 23) | mantissa
+                            uint32_t sgn = (aal ^ bal) & 0x80000000u;
+                            int Exp = int(ea + eb) - 127;
+                            uint32_t pbits;
+                            if (ea == 0 || eb == 0 || Exp <= 0) {
+                                pbits = 0u;                                    // +0 (C4, C6, C8)
+                            } else if (Exp >= 255) {
+                                pbits = sgn | 0x7F800000u;                     // +-Inf (C6)
+                            } else {
+                                int E = Exp + int((ent >> 23) & 1u);           // Exp + Carry (C3)
+                                pbits = (E >= 255) ? (sgn | 0x7F800000u)       // C5
+                                                   : (sgn | (uint32_t(E) << 23) | (ent & 0x7FFFFFu));
+                            }
+                            acc[r][c] = add_ftz(acc[r][c], __uint_as_float(pbits));
+                        }
+                    }
+                }
+            }
+        }
+
+        // epilogue: this thread's TM x TN outputs (split partials go to the workspace)
+        const SubP &S = p.sub[T.s];
+        const bool split_out = S.splits > 1;
+        float *Cb = split_out ? p.ws + S.ws_offset + int64_t(T.split) * S.M * p.N : p.C;
+#pragma unroll
+        for (int r = 0; r < TM; r++) {
+            int row = T.m0 + warp * TM + r;
+            if (row >= S.M) continue;
+            float *dst = Cb + (split_out ? int64_t(row) * p.N : opa.out_row(T.s, row, p.ldc));
+#pragma unroll
+            for (int c = 0; c < TN; c++) {
+                int col = T.n0 + lane * TN + c;
+                if (col >= p.N) continue;
+                dst[col] = (p.accumulate && !split_out) ? (dst[col] + acc[r][c]) : acc[r][c];
+            }
+        }
+    }
+}
+
+// Deterministic split-K reduction for sub-problem blockIdx.y:
+// C[out_row(s, i)][j] (+)= sum over splits, in increasing split order.
+template <class OpA>
+__global__ void splitk_reduce_kernel(const __grid_constant__ KParams p, const __grid_constant__ OpA opa)
+{
+    const SubP &S = p.sub[blockIdx.y];
+    if (S.splits <= 1) return;
+    const float *ws = p.ws + S.ws_offset;
+    const int64_t total = int64_t(S.M) * p.N;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        float s = 0.0f;
+        for (int k = 0; k < S.splits; k++) s += ws[int64_t(k) * total + e];
+        int i = int(e / p.N), j = int(e - int64_t(i) * p.N);
+        float *dst = p.C + opa.out_row(blockIdx.y, i, p.ldc) + j;
+        *dst = p.accumulate ? (*dst + s) : s;
+    }
+}
+
+}  // namespace dev
+}  // namespace amsim

@@ -114,7 +114,7 @@ uint64_t amsim_launch_count(void) { return g_launches.load(); }
 
 amsim_status amsim_set_path_policy(int policy)
 {
-    if (policy != 0 && policy != 1) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be 0 or 1");
+    if (policy < 0 || policy > 3) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 3]");
     g_policy.store(policy);
     return AMSIM_OK;
 }
