@@ -95,8 +95,10 @@ amsim_status amsim_lut_from_entries(const uint32_t *entries, int m_bits, amsim_l
  * valid until amsim_lut_destroy). */
 amsim_status amsim_lut_entries(const amsim_lut *lut, const uint32_t **entries, size_t *count);
 
-/* m, and the device entry width the kernels use: 16 when every entry's low 8
- * mantissa bits are zero (carry + 15 fraction bits suffice), else 32. */
+/* m, and the device entry width the kernels use: 8 when every entry's low 16
+ * mantissa bits are zero (carry + 7 fraction bits suffice, e.g. Mitchell at
+ * m <= 7), else 16 when every entry's low 8 bits are zero (carry + 15 fraction
+ * bits), else 32.  The width changes the kernels' speed, never their bits. */
 amsim_status amsim_lut_info(const amsim_lut *lut, int *m_bits, int *device_entry_bits);
 
 /* LUT binary file ("LUTs are written into binary files"),
@@ -190,7 +192,10 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
  *   bit 1 -- never split K: every output is then the FP32 sum from +0 in
  *            increasing k, bit-identical to a sequential reference (default:
  *            the tile planner may split K to balance the SMs; partials are
- *            reduced in a fixed order, so results stay deterministic). */
+ *            reduced in a fixed order, so results stay deterministic);
+ *   bit 2 -- use the 32-bit device table layout even when the table fits 8
+ *            or 16 bits (tests: the layout changes speed, never bits).
+ * Errors: AMSIM_ERR_INVALID_ARG outside [0, 7]. */
 amsim_status amsim_set_path_policy(int policy);
 
 /* Kernel launches issued by this library in this process (all entry points). */
@@ -198,7 +203,7 @@ uint64_t amsim_launch_count(void);
 
 /* Roofline instrument: shared-memory LUT-lookup microbenchmark.  Runs the
  * lookup pattern of the GEMM inner loop (lanes of a warp share the table
- * row, columns drawn from `b_idx`; m bits, `entry_bits` 16 or 32) for
+ * row, columns drawn from `b_idx`; m bits, `entry_bits` 8, 16 or 32) for
  * `iters` iterations on every SM and writes the achieved lookups per second
  * to *lookups_per_s (synchronises `stream`). */
 amsim_status amsim_bench_lut_lookup(int m_bits, int entry_bits, int iters, const uint32_t *b_idx_host,

@@ -15,7 +15,8 @@
 //  * The 32 lanes of a warp share the A element (same table row) and take
 //    32*TN different B columns, so one warp-wide lookup touches a single
 //    2^m-entry row (m = 7, 16-bit entries: 64 words on 32 banks, <= 2
-//    wavefronts).
+//    wavefronts; 8-bit entries -- tables whose mantissas fit 7 bits, e.g.
+//    Mitchell at m <= 7: 32 words, 1 wavefront).
 //  * Fast path per product: e = LUT[rowoff(a) + off(b)]; x = e*mul_b + alpha_b
 //    (integer add into the exponent field: x = +-(1.mant*2^carry)*2^(eb-127);
 //    mul_b = 0 makes x = +-0 when b is zero); acc = fma.rn.ftz(x, alpha_a, acc).
@@ -96,7 +97,9 @@ template <int EB>
 __device__ __forceinline__ uint32_t lds_entry(uint32_t addr)
 {
     uint32_t v;
-    if constexpr (EB == 16)
+    if constexpr (EB == 8)
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    else if constexpr (EB == 16)
         asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
     else
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -392,9 +395,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     const int m = p.m_bits;
     const int shift = 23 - m;
     const uint32_t mask = (1u << m) - 1u;
-    constexpr int ebytes_log2 = EB == 16 ? 1 : 2;
+    constexpr int ebytes_log2 = EB == 8 ? 0 : (EB == 16 ? 1 : 2);
     const uint32_t lut_base = smem_u32(lut_s);
-    constexpr uint32_t MULV = EB == 16 ? 256u : 1u;
+    // entry << (32 - EB) restores the Alg. 1 layout (carry << 23) | mantissa
+    constexpr uint32_t MULV = EB == 8 ? 65536u : (EB == 16 ? 256u : 1u);
     const float *dummy = reinterpret_cast<const float *>(p.lut);  // valid global address for 0-byte copies
 
     struct Tile {

@@ -51,6 +51,39 @@ static inline float compose(uint32_t sign, int E, uint32_t mant)
     return flt(sign | (uint32_t(E) << 23) | (mant & 0x7FFFFFu));
 }
 
+// Upload the table for the current device in layout `eb` (8, 16 or 32 bits).
+static amsim_status upload(amsim_lut *lut, int dev, int eb, DeviceTable &t)
+{
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return set_error(AMSIM_ERR_UNSUPPORTED, "libamsim is built for sm_100a (B200) only; device is sm_" +
+                                                    std::to_string(major) + std::to_string(minor));
+    size_t n = lut->entries.size();
+    size_t bytes = n * (eb / 8);
+    std::vector<uint8_t> host(bytes);
+    if (eb == 8) {
+        for (size_t i = 0; i < n; i++) host[i] = uint8_t(lut->entries[i] >> 16);
+    } else if (eb == 16) {
+        uint16_t *h16 = reinterpret_cast<uint16_t *>(host.data());
+        for (size_t i = 0; i < n; i++) h16[i] = uint16_t(lut->entries[i] >> 8);
+    } else {
+        std::memcpy(host.data(), lut->entries.data(), bytes);
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return set_error(AMSIM_ERR_NOMEM, std::string("cudaMalloc(LUT): ") + cudaGetErrorString(e));
+    e = cudaMemcpy(p, host.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return set_error(AMSIM_ERR_CUDA, std::string("LUT upload: ") + cudaGetErrorString(e));
+    }
+    t.ptr = p;
+    t.bytes = bytes;
+    return AMSIM_OK;
+}
+
 amsim_status device_table(const amsim_lut *lut_c, const void **ptr, int *entry_bits)
 {
     amsim_lut *lut = const_cast<amsim_lut *>(lut_c);
@@ -58,46 +91,27 @@ amsim_status device_table(const amsim_lut *lut_c, const void **ptr, int *entry_b
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return set_error(AMSIM_ERR_UNSUPPORTED, std::string("no CUDA device: ") + cudaGetErrorString(e));
     if (dev < 0 || dev >= kMaxDevices) return set_error(AMSIM_ERR_UNSUPPORTED, "device index out of range");
+    // policy bit 2: the 32-bit layout whatever the table's width (tests prove the width never changes bits)
+    const bool wide = (path_policy() & 4) != 0 && lut->device_entry_bits != 32;
+    const int eb = wide ? 32 : lut->device_entry_bits;
     std::lock_guard<std::mutex> g(lut->mu);
-    DeviceTable &t = lut->dev[dev];
+    DeviceTable &t = wide ? lut->dev_wide[dev] : lut->dev[dev];
     if (!t.ptr) {
-        int major = 0, minor = 0;
-        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-        if (major != 10 || minor != 0)
-            return set_error(AMSIM_ERR_UNSUPPORTED, "libamsim is built for sm_100a (B200) only; device is sm_" +
-                                                        std::to_string(major) + std::to_string(minor));
-        size_t n = lut->entries.size();
-        size_t bytes = n * (lut->device_entry_bits / 8);
-        std::vector<uint8_t> host(bytes);
-        if (lut->device_entry_bits == 16) {
-            uint16_t *h16 = reinterpret_cast<uint16_t *>(host.data());
-            for (size_t i = 0; i < n; i++) h16[i] = uint16_t(lut->entries[i] >> 8);
-        } else {
-            std::memcpy(host.data(), lut->entries.data(), bytes);
-        }
-        void *p = nullptr;
-        e = cudaMalloc(&p, bytes);
-        if (e != cudaSuccess) return set_error(AMSIM_ERR_NOMEM, std::string("cudaMalloc(LUT): ") + cudaGetErrorString(e));
-        e = cudaMemcpy(p, host.data(), bytes, cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) {
-            cudaFree(p);
-            return set_error(AMSIM_ERR_CUDA, std::string("LUT upload: ") + cudaGetErrorString(e));
-        }
-        t.ptr = p;
-        t.bytes = bytes;
+        amsim_status s = upload(lut, dev, eb, t);
+        if (s != AMSIM_OK) return s;
     }
     *ptr = t.ptr;
-    *entry_bits = lut->device_entry_bits;
+    *entry_bits = eb;
     return AMSIM_OK;
 }
 
 static void finalize_lut(amsim_lut *lut)
 {
-    bool ok16 = true;
-    for (uint32_t e : lut->entries)
-        if (e & 0xFFu) { ok16 = false; break; }
-    lut->device_entry_bits = ok16 ? 16 : 32;
+    // Narrowest device layout that holds every entry exactly: 8 bits (carry |
+    // 7 mantissa bits, e.g. Mitchell at m <= 7), 16 bits (carry | 15), else 32.
+    uint32_t low = 0;
+    for (uint32_t e : lut->entries) low |= e;
+    lut->device_entry_bits = (low & 0xFFFFu) == 0 ? 8 : ((low & 0xFFu) == 0 ? 16 : 32);
 }
 
 }  // namespace amsim
@@ -114,7 +128,7 @@ uint64_t amsim_launch_count(void) { return g_launches.load(); }
 
 amsim_status amsim_set_path_policy(int policy)
 {
-    if (policy < 0 || policy > 3) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 3]");
+    if (policy < 0 || policy > 7) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 7]");
     g_policy.store(policy);
     return AMSIM_OK;
 }
@@ -315,9 +329,11 @@ void amsim_lut_destroy(amsim_lut *lut)
     int cur = -1;
     cudaGetDevice(&cur);
     for (int d = 0; d < kMaxDevices; d++) {
-        if (lut->dev[d].ptr) {
-            cudaSetDevice(d);
-            cudaFree(lut->dev[d].ptr);
+        for (amsim::DeviceTable *t : {&lut->dev[d], &lut->dev_wide[d]}) {
+            if (t->ptr) {
+                cudaSetDevice(d);
+                cudaFree(t->ptr);
+            }
         }
     }
     if (cur >= 0) cudaSetDevice(cur);

@@ -14,8 +14,9 @@ namespace amsim {
 constexpr int kMaxDevices = 64;
 
 // Device copy of a table in the kernels' layout: row k (first operand) is
-// 2^m consecutive entries; 16-bit entries hold bits 23..8 of the Alg. 1 entry
-// (carry | top 15 mantissa bits) when every entry's low 8 bits are zero.
+// 2^m consecutive entries; 8-bit entries hold bits 23..16 of the Alg. 1 entry
+// (carry | top 7 mantissa bits) when every entry's low 16 bits are zero,
+// 16-bit entries bits 23..8 when every entry's low 8 bits are zero.
 struct DeviceTable {
     void *ptr = nullptr;
     size_t bytes = 0;
@@ -26,9 +27,10 @@ struct DeviceTable {
 struct amsim_lut {
     int m = 0;
     std::vector<uint32_t> entries;   // Alg. 1 layout: (carry << 23) | mantissa
-    int device_entry_bits = 32;      // 16 if every entry has (e & 0xFF) == 0
+    int device_entry_bits = 32;      // 8 if every (e & 0xFFFF) == 0, else 16 if every (e & 0xFF) == 0
     std::mutex mu;
-    amsim::DeviceTable dev[amsim::kMaxDevices];
+    amsim::DeviceTable dev[amsim::kMaxDevices];        // narrowest layout
+    amsim::DeviceTable dev_wide[amsim::kMaxDevices];   // 32-bit layout (policy bit 2, tests)
 };
 
 namespace amsim {

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(BENCH_NT, 1) lut_bench_kernel(const void *lut,
     const uint4 *src = reinterpret_cast<const uint4 *>(lut);
     for (uint32_t i = threadIdx.x; i < lut_bytes / 16; i += BENCH_NT) reinterpret_cast<uint4 *>(smem)[i] = src[i];
     __syncthreads();
-    constexpr int ebl = EB == 16 ? 1 : 2;
+    constexpr int ebl = EB == 8 ? 0 : (EB == 16 ? 1 : 2);
     const uint32_t base = smem_u32(smem);
     const int warp = threadIdx.x >> 5;
     const uint32_t rmask = (1u << m) - 1u;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(BENCH_NT, 1) lut_bench_kernel(const void *lut,
 #pragma unroll
             for (int c = 0; c < 4; c++) {
                 uint32_t e = lds_entry<EB>(aof + bof[c]);
-                acc[r][c] = fma_ftz(__uint_as_float(e * 256u + 0x3F800000u), 1.0f, acc[r][c]);
+                acc[r][c] = fma_ftz(__uint_as_float(e * (EB == 8 ? 65536u : 256u) + 0x3F800000u), 1.0f, acc[r][c]);
             }
         }
     }
@@ -282,7 +282,7 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
         }
         p.ws = ws;
     }
-    amsim_status s = eb == 16 ? launch_eb<16>(p, a, b, st) : launch_eb<32>(p, a, b, st);
+    amsim_status s = eb == 8 ? launch_eb<8>(p, a, b, st) : (eb == 16 ? launch_eb<16>(p, a, b, st) : launch_eb<32>(p, a, b, st));
     if (s == AMSIM_OK && p.ws_elems > 0) {
         int64_t maxmn = 0;
         for (int i = 0; i < p.nsub; i++) maxmn = std::max<int64_t>(maxmn, int64_t(p.sub[i].M) * p.N);
@@ -534,7 +534,8 @@ amsim_status amsim_bench_lut_lookup(int m_bits, int entry_bits, int iters, const
                                     double *lookups_per_s, amsim_stream_t stream)
 {
     clear_error();
-    if (m_bits < 1 || m_bits > 8 || (entry_bits != 16 && entry_bits != 32) || iters <= 0 || !b_idx_host || !n_idx ||
+    if (m_bits < 1 || m_bits > 8 || (entry_bits != 8 && entry_bits != 16 && entry_bits != 32) || iters <= 0 ||
+        !b_idx_host || !n_idx ||
         !lookups_per_s)
         return set_error(AMSIM_ERR_INVALID_ARG, "amsim_bench_lut_lookup: bad argument");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -557,7 +558,10 @@ amsim_status amsim_bench_lut_lookup(int m_bits, int entry_bits, int iters, const
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         auto launch = [&]() {
-            if (entry_bits == 16) {
+            if (entry_bits == 8) {
+                cudaFuncSetAttribute(lut_bench_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+                lut_bench_kernel<8><<<sms, BENCH_NT, bytes, st>>>(tab, bytes, m_bits, idx, int(n_idx), iters, out);
+            } else if (entry_bits == 16) {
                 cudaFuncSetAttribute(lut_bench_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
                 lut_bench_kernel<16><<<sms, BENCH_NT, bytes, st>>>(tab, bytes, m_bits, idx, int(n_idx), iters, out);
             } else {

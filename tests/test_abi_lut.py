@@ -73,7 +73,13 @@ def test_m1_exact_table(built):
 def test_device_entry_width(built):
     # exact at m=7: products of 8-bit significands need 15 fraction bits -> 16-bit entries
     assert am.Lut.build("exact", 7).info() == (7, 16)
-    assert am.Lut.build("mitchell", 7).info() == (7, 16)
+    assert am.Lut.build("mbm", 7).info() == (7, 16)
+    # Mitchell: carry + the m-bit sum of the operand mantissas -> 8-bit entries up to m = 7
+    assert am.Lut.build("mitchell", 7).info() == (7, 8)
+    assert am.Lut.build("mitchell", 8).info() == (8, 16)
+    # exact at m = 3: (8+k)(8+j)/64 has 6 fraction bits -> 8-bit entries
+    assert am.Lut.build("exact", 3).info() == (3, 8)
+    assert am.Lut.build("exact", 4).info() == (4, 16)
     assert am.Lut.build("exact", 11).info() == (11, 32)
 
 

@@ -296,6 +296,33 @@ def test_conv_vs_oracle(am, luts, orc, shape, which, model):
     assert_bits(got, res.c32, f"{which} {shape} vs c32")
 
 
+@pytest.mark.parametrize("model,m,width", [("mitchell", 7, 8), ("exact", 3, 8), ("mbm", 7, 16), ("exact", 6, 16)])
+def test_entry_layout_never_changes_bits(am, luts, orc, model, m, width):
+    """The narrow device layouts (8-bit: carry | 7 mantissa bits; 16-bit) give
+    the same bits as the 32-bit Alg. 1 layout (policy bit 2), for GEMM and all
+    three conv passes; and the narrow layout matches the oracle's c32."""
+    lut = luts(model, m)
+    assert lut.info() == (m, width)
+    A = inp.normal((150, 90), 71)
+    B = inp.normal((90, 140), 72)
+    shape = (2, 14, 14, 16, 72, 3, 3, 2, 1)
+    x, w, dy, OH, OW = _conv_tensors(shape, 73)
+    d = am.conv_desc(*shape)
+    outs = {}
+    for pol in (0, 4, 2, 6):
+        am.amsim_set_path_policy(pol)
+        try:
+            outs[pol] = [run_gemm(am, lut, A, B)] + [_run_conv(am, lut, d, x, w, dy, k)
+                                                      for k in ("fwd", "dgrad", "wgrad")]
+        finally:
+            am.amsim_set_path_policy(0)
+    for i in range(4):
+        assert_bits(outs[0][i], outs[4][i], f"{model} m={m} part {i} split")
+        assert_bits(outs[2][i], outs[6][i], f"{model} m={m} part {i} exact order")
+    assert_bits(outs[2][0], orc.gemm(A, B, model, m).c32, "gemm vs c32")
+    assert_bits(outs[2][1], orc.conv_fwd(orc.conv_desc(*shape), x, w, model, m).c32, "fwd vs c32")
+
+
 def test_conv_operand_order_asymmetric(am, orc):
     """An asymmetric table must give a = x for fwd/wgrad and a = dy for dgrad
     (reading C11).  The user model is a Python callback passed through the
@@ -395,9 +422,10 @@ def test_resnet50_full_size_sampled(am, luts, orc, name):
     torch.cuda.empty_cache()
 
 
-def test_lut_lookup_microbench(am):
+@pytest.mark.parametrize("width", [8, 16, 32])
+def test_lut_lookup_microbench(am, width):
     idx = inp.rng(3).integers(0, 128, 1 << 16).astype(np.uint32)
-    r = am.amsim_bench_lut_lookup(7, 16, idx, iters=256)
+    r = am.amsim_bench_lut_lookup(7, width, idx, iters=256)
     assert r > 1e11
 
 
