@@ -34,6 +34,10 @@
  *     synchronisation.
  *   - No CPU fallback: without an sm_100 device every compute call returns
  *     AMSIM_ERR_UNSUPPORTED.
+ *   - Table placement: a table that fits shared memory (every m <= 7, and
+ *     m = 8 with 8/16-bit entries) is replicated in each SM's shared memory;
+ *     larger ones (m = 8 with 32-bit entries, m = 9..11: 512 KB - 16 MB) are
+ *     read from global memory and stay L2-resident.  Same bits either way.
  *   - Results are deterministic: the same call on the same inputs gives the
  *     same bits (fixed accumulation order per output; split-K partials are
  *     reduced in a fixed order).
@@ -197,6 +201,24 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
  *            or 16 bits (tests: the layout changes speed, never bits).
  * Errors: AMSIM_ERR_INVALID_ARG outside [0, 7]. */
 amsim_status amsim_set_path_policy(int policy);
+
+/* Multiply mode (process-wide, default AMSIM_MUL_LUT).  The two other modes
+ * are measurement instruments for the paper's comparisons, not AMSim:
+ *   AMSIM_MUL_LUT    -- AMSim: the table lookup of Alg. 2 (the product path);
+ *   AMSIM_MUL_NATIVE -- the same GEMM / conv kernels with the native IEEE FP32
+ *                       multiply-add of the UNtruncated operands (ApproxTrain
+ *                       with native multiplication, "ATnG");
+ *                       the table is not read;
+ *   AMSIM_MUL_DIRECT -- the table's functional model evaluated per product on
+ *                       the device with no table ("direct simulation",
+ *                       PAPER.md:345-349, 398); same bits as AMSIM_MUL_LUT.
+ *                       Only for tables built by amsim_lut_build from a
+ *                       built-in model, else AMSIM_ERR_UNSUPPORTED at the call.
+ * Errors: AMSIM_ERR_INVALID_ARG for an unknown mode. */
+#define AMSIM_MUL_LUT 0
+#define AMSIM_MUL_NATIVE 1
+#define AMSIM_MUL_DIRECT 2
+amsim_status amsim_set_multiply_mode(int mode);
 
 /* Kernel launches issued by this library in this process (all entry points). */
 uint64_t amsim_launch_count(void);

@@ -51,8 +51,11 @@ EXPORTS = [
     "amsim_lut_load", "amsim_lut_destroy", "amsim_last_error", "amsim_model_exact", "amsim_model_mitchell",
     "amsim_model_mbm", "amsim_gemm", "amsim_conv2d_fwd", "amsim_conv2d_bwd_data",
     "amsim_conv2d_bwd_filter_workspace", "amsim_conv2d_bwd_filter", "amsim_set_path_policy",
-    "amsim_launch_count", "amsim_bench_lut_lookup", "amsim_abi_version",
+    "amsim_launch_count", "amsim_bench_lut_lookup", "amsim_abi_version", "amsim_set_multiply_mode",
 ]
+
+# amsim_set_multiply_mode values (include/amsim.h)
+AMSIM_MUL_LUT, AMSIM_MUL_NATIVE, AMSIM_MUL_DIRECT = 0, 1, 2
 
 _lib = None
 
@@ -84,6 +87,7 @@ def lib():
     L.amsim_conv2d_bwd_filter_workspace.argtypes = [vp, ctypes.POINTER(ConvDesc), ctypes.POINTER(ctypes.c_size_t)]
     L.amsim_conv2d_bwd_filter.argtypes = [vp, ctypes.POINTER(ConvDesc), vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.amsim_set_path_policy.argtypes = [i32]
+    L.amsim_set_multiply_mode.argtypes = [i32]
     L.amsim_launch_count.restype = ctypes.c_uint64
     L.amsim_bench_lut_lookup.argtypes = [i32, i32, i32, u32p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double), vp]
     L.amsim_abi_version.restype = i32
@@ -241,6 +245,24 @@ def amsim_conv2d_bwd_filter(lut: Lut, d: ConvDesc, x, dy, dw, workspace=None, st
 
 def amsim_set_path_policy(policy: int):
     _check(lib().amsim_set_path_policy(policy), "amsim_set_path_policy")
+
+
+def amsim_set_multiply_mode(mode: int):
+    _check(lib().amsim_set_multiply_mode(mode), "amsim_set_multiply_mode")
+
+
+class multiply_mode:
+    """Context manager: run the enclosed calls in AMSIM_MUL_NATIVE / _DIRECT
+    (measurement instruments), restoring AMSIM_MUL_LUT afterwards."""
+
+    def __init__(self, mode: int):
+        self.mode = mode
+
+    def __enter__(self):
+        amsim_set_multiply_mode(self.mode)
+
+    def __exit__(self, *a):
+        amsim_set_multiply_mode(AMSIM_MUL_LUT)
 
 
 def amsim_launch_count() -> int:

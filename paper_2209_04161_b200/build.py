@@ -19,10 +19,14 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES = [
     ("amsim_host.cpp", "g++"),
-    ("amsim_kernels.cu", "nvcc"),
+    ("amsim_gemm.cu", "nvcc"),
+    ("amsim_conv_fwd.cu", "nvcc"),
+    ("amsim_conv_dgrad.cu", "nvcc"),
+    ("amsim_conv_wgrad.cu", "nvcc"),
+    ("amsim_bench.cu", "nvcc"),
 ]
 HEADERS = [os.path.join(CSRC, "amsim_internal.h"), os.path.join(CSRC, "amsim_device.cuh"),
-           os.path.join(ROOT, "include", "amsim.h")]
+           os.path.join(CSRC, "amsim_dispatch.cuh"), os.path.join(ROOT, "include", "amsim.h")]
 
 
 def _newer(target: str, deps) -> bool:
@@ -72,13 +76,21 @@ def build_variant(tag: str, defines) -> str:
     os.makedirs(vdir, exist_ok=True)
     host_o = os.path.join(BUILD, "amsim_host.cpp.o")
     build()  # host object
-    ko = os.path.join(vdir, f"kernels_{tag}.o")
     so = os.path.join(vdir, f"libamsim_{tag}.so")
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-           *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
-           "-c", os.path.join(CSRC, "amsim_kernels.cu"), "-o", ko]
-    subprocess.run(cmd, check=True)
-    subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", so, host_o, ko, "-lpthread", "-ldl", "-lrt"],
+    objs, procs = [host_o], []
+    for src, tool in SOURCES:
+        if tool != "nvcc":
+            continue
+        ko = os.path.join(vdir, f"{src}_{tag}.o")
+        objs.append(ko)
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+               *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+               "-c", os.path.join(CSRC, src), "-o", ko]
+        procs.append(subprocess.Popen(cmd))
+    for p in procs:
+        if p.wait() != 0:
+            raise RuntimeError(f"variant build failed: {p.args}")
+    subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", so, *objs, "-lpthread", "-ldl", "-lrt"],
                    check=True)
     return so
 

@@ -1,0 +1,43 @@
+// libamsim: conv preceding-layer gradient, Alg. 4 l.6-8 (C-ABI entry points of include/amsim.h).
+// Citations "PAPER.md:L" are lines of /root/reference/PAPER.md.
+#include "amsim_dispatch.cuh"
+
+using namespace amsim;
+using namespace amsim::dev;
+
+extern "C" {
+
+amsim_status amsim_conv2d_bwd_data(const amsim_lut *lut, const amsim_conv2d_desc *d, const float *dy,
+                                   const float *w, float *dx, amsim_stream_t stream)
+{
+    clear_error();
+    if (!lut) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_data: null lut");
+    amsim_status s = check_desc(d);
+    if (s != AMSIM_OK) return s;
+    if (d->N == 0) return AMSIM_OK;
+    if (!dy || !w || !dx) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_data: null tensor");
+    DgDY a{};
+    DgW b{};
+    init_geom(a.g, d);
+    Problem pr;
+    dgrad_phases(d, pr, a.ph);
+    a.dy = dy;
+    a.fK.init(uint32_t(d->K));
+    b.w = w;
+    b.g = a.g;
+    b.fK = a.fK;
+    std::memcpy(b.ph, a.ph, sizeof(a.ph));
+    KParams p{};
+    int eb = 32;
+    s = prepare(lut, p, pr, eb);
+    if (s != AMSIM_OK) return s;
+    bool v = d->K % 4 == 0;
+    p.da = OpDesc{1, (v && aligned16(dy)) ? 2 : 0};
+    p.db = OpDesc{1, (v && aligned16(w)) ? 2 : 0};
+    p.C = dx;
+    p.ldc = d->C;
+    p.accumulate = 0;
+    return run(eb, p, a, b, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// libamsim: conv weight gradient, Alg. 4 l.4-5 (C-ABI entry points of include/amsim.h).
+// Citations "PAPER.md:L" are lines of /root/reference/PAPER.md.
+#include "amsim_dispatch.cuh"
+
+using namespace amsim;
+using namespace amsim::dev;
+
+extern "C" {
+
+static amsim_status wgrad_plan(const amsim_lut *lut, const amsim_conv2d_desc *d, KParams &p, ConvGeom &g, int &eb)
+{
+    init_geom(g, d);
+    Problem pr;
+    pr.N = d->K;
+    pr.M[0] = d->R * d->S * d->C;
+    pr.K[0] = d->N * g.OH * g.OW;
+    pr.max_splits = 1024;
+    return prepare(lut, p, pr, eb);
+}
+
+amsim_status amsim_conv2d_bwd_filter_workspace(const amsim_lut *lut, const amsim_conv2d_desc *d, size_t *bytes)
+{
+    clear_error();
+    if (!lut || !bytes) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter_workspace: null argument");
+    amsim_status s = check_desc(d);
+    if (s != AMSIM_OK) return s;
+    KParams p{};
+    ConvGeom g;
+    int eb;
+    s = wgrad_plan(lut, d, p, g, eb);
+    if (s != AMSIM_OK) return s;
+    *bytes = size_t(p.ws_elems) * sizeof(float);
+    return AMSIM_OK;
+}
+
+amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_desc *d, const float *x,
+                                     const float *dy, float *dw, void *workspace, size_t workspace_bytes,
+                                     amsim_stream_t stream)
+{
+    clear_error();
+    if (!lut) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter: null lut");
+    amsim_status s = check_desc(d);
+    if (s != AMSIM_OK) return s;
+    if (!x || !dy || !dw) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter: null tensor");
+    KParams p{};
+    ConvGeom g;
+    int eb;
+    s = wgrad_plan(lut, d, p, g, eb);
+    if (s != AMSIM_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const SubP &S = p.sub[0];
+    if (S.K == 0) {
+        fill_zero_kernel<<<64, 256, 0, st>>>(dw, S.M, p.N, p.N);
+        count_launch();
+        return cuda_check(cudaGetLastError(), "fill_zero launch");
+    }
+    size_t need = size_t(p.ws_elems) * sizeof(float);
+    if (need > 0 && (!workspace || workspace_bytes < need))
+        return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter: workspace too small (need " +
+                                                    std::to_string(need) + " bytes)");
+    WgX a{x, g, S.M, S.K};
+    GemmOp b{dy, d->K, p.N, S.K, 0};
+    p.da = OpDesc{0, (d->C % 4 == 0 && aligned16(x)) ? 2 : 0};
+    p.db = OpDesc{0, (d->K % 4 == 0 && aligned16(dy)) ? 2 : 0};
+    p.C = dw;
+    p.ldc = p.N;
+    p.accumulate = 0;
+    return run(eb, p, a, b, st, static_cast<float *>(workspace));
+}
+
+}  // extern "C"

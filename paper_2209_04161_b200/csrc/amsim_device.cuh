@@ -93,16 +93,29 @@ __device__ __forceinline__ float add_ftz(float a, float b)
     return d;
 }
 
-template <int EB>
-__device__ __forceinline__ uint32_t lds_entry(uint32_t addr)
+// Table entry at byte offset `addr`: a shared-memory address (GL = false) or
+// an offset from `gbase`, the global (L2-resident) table (GL = true: tables
+// too large for shared memory, m >= 8).
+template <int EB, bool GL = false>
+__device__ __forceinline__ uint32_t lut_entry(uint32_t addr, const unsigned char *gbase)
 {
     uint32_t v;
-    if constexpr (EB == 8)
-        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
-    else if constexpr (EB == 16)
-        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
-    else
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    if constexpr (!GL) {
+        if constexpr (EB == 8)
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+        else if constexpr (EB == 16)
+            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+        else
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    } else {
+        const unsigned char *q = gbase + addr;
+        if constexpr (EB == 8)
+            asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(q));
+        else if constexpr (EB == 16)
+            asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(v) : "l"(q));
+        else
+            asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(q));
+    }
     return v;
 }
 
@@ -152,6 +165,8 @@ struct KParams {
     int m_bits;
     uint32_t lut_bytes;
     int policy;           // 1 = force the careful path
+    int lut_global;       // table read from global memory / L2 (too large for shared memory)
+    int mul;              // MulMode
 };
 
 // ---------------------------------------------------------------------------
@@ -338,7 +353,7 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
 
 // Decode one raw operand tile into (alpha, offset) arrays laid out [BK][rows];
 // tracks min / max exponent fields over nonzero elements.
-template <int NT, int ROWS>
+template <int NT, int ROWS, bool RAW_ALPHA = false>
 __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, uint32_t *al, uint32_t *off, int shift,
                                                uint32_t mask, int off_shift, uint32_t off_base, uint32_t &emin,
                                                uint32_t &emax)
@@ -352,7 +367,7 @@ __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, ui
             float v = kcontig ? raw[i * (BK + RAW_PAD) + kk] : raw[kk * ROWS + i];
             uint32_t u = __float_as_uint(v);
             uint32_t ex = (u >> 23) & 0xFFu;
-            al[e] = u & 0xFF800000u;
+            al[e] = RAW_ALPHA ? u : (u & 0xFF800000u);
             off[e] = off_base + (((u >> shift) & mask) << off_shift);
             if (ex) {
                 emin = min(emin, ex);
@@ -362,7 +377,41 @@ __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, ui
     }
 }
 
-template <class Cf, int EB, class OpA, class OpB>
+// Multiply modes (amsim_set_multiply_mode): the AMSim table lookup (the
+// product path), or -- measurement instruments for the paper's comparisons --
+// the native FP32 multiply (ATnG analog) and direct
+// per-product evaluation of a built-in functional model with no table
+// (PAPER.md:345-349, 398).
+enum MulMode { MUL_LUT = 0, MUL_NATIVE = 1, MUL_DIRECT_EXACT = 2, MUL_DIRECT_MITCHELL = 3, MUL_DIRECT_MBM = 4 };
+
+// Direct evaluation of a model's Alg. 1 entry (carry << 23) | mantissa from
+// the operands' truncated fractions.  MUL_DIRECT_EXACT receives the fractions
+// as floats 1.f (exponent field 127), the others the in-place 23-bit
+// fractions.  Each mirrors the host model of the same name (amsim_host.cpp).
+template <int MUL>
+__device__ __forceinline__ uint32_t direct_entry(uint32_t oa, uint32_t ob)
+{
+    if constexpr (MUL == MUL_DIRECT_EXACT) {
+        // (1.fa)(1.fb) in [1, 4) is exact in FP32 for m <= 11; exponent 127 or 128
+        return __float_as_uint(__fmul_rn(__uint_as_float(oa), __uint_as_float(ob))) - 0x3F800000u;
+    } else if constexpr (MUL == MUL_DIRECT_MITCHELL) {
+        return oa + ob;  // fa + fb: the carry lands in bit 23
+    } else {
+        const uint32_t one = 1u << 23;
+        uint32_t s = oa + ob;
+        if (s < one) {
+            uint32_t sig = one + s + (5u << 17);  // 1 + fa + fb + 5/64
+            if (sig >= 2 * one) {                 // renormalise (round to nearest even): carry
+                uint32_t h = sig >> 1;
+                return h + (sig & h & 1u);        // in [2^23, 2^24): (1 << 23) | mantissa
+            }
+            return sig - one;
+        }
+        return min(s + (5u << 16), 2 * one - (1u << 8));  // (fa + fb) + 5/128, saturated; carry = 1
+    }
+}
+
+template <class Cf, int EB, class OpA, class OpB, bool GL = false, int MUL = MUL_LUT>
 __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_constant__ KParams p,
                                                              const __grid_constant__ OpA opa,
                                                              const __grid_constant__ OpB opb)
@@ -371,7 +420,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t lut_pad = (p.lut_bytes + 127u) & ~127u;
+    const uint32_t lut_pad = (GL || MUL != MUL_LUT) ? 0u : ((p.lut_bytes + 127u) & ~127u);
+    const unsigned char *lut_g = reinterpret_cast<const unsigned char *>(p.lut);
     unsigned char *lut_s = smem;
     float *raw = reinterpret_cast<float *>(smem + lut_pad);
     uint32_t *dec = reinterpret_cast<uint32_t *>(raw + Cf::RAW_STAGE * STAGES);
@@ -379,7 +429,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     uint64_t *bars = reinterpret_cast<uint64_t *>(wflags + NWARPS * 2);
 
     // table -> shared memory, once per persistent CTA
-    {
+    if constexpr (!GL && MUL == MUL_LUT) {
         const uint4 *src = reinterpret_cast<const uint4 *>(p.lut);
         uint4 *dst = reinterpret_cast<uint4 *>(lut_s);
         for (uint32_t i = tid; i < p.lut_bytes / 16; i += NT) dst[i] = src[i];
@@ -396,9 +446,14 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     const int shift = 23 - m;
     const uint32_t mask = (1u << m) - 1u;
     constexpr int ebytes_log2 = EB == 8 ? 0 : (EB == 16 ? 1 : 2);
-    const uint32_t lut_base = smem_u32(lut_s);
+    const uint32_t lut_base = GL ? 0u : smem_u32(lut_s);
     // entry << (32 - EB) restores the Alg. 1 layout (carry << 23) | mantissa
-    constexpr uint32_t MULV = EB == 8 ? 65536u : (EB == 16 ? 256u : 1u);
+    constexpr uint32_t MULV = MUL != MUL_LUT ? 1u : (EB == 8 ? 65536u : (EB == 16 ? 256u : 1u));
+    // decode: table byte offsets (LUT) or in-place truncated fractions (direct)
+    const int a_off_shift = MUL == MUL_LUT ? m + ebytes_log2 : shift;
+    const int b_off_shift = MUL == MUL_LUT ? ebytes_log2 : shift;
+    const uint32_t a_off_base = MUL == MUL_LUT ? lut_base : (MUL == MUL_DIRECT_EXACT ? 0x3F800000u : 0u);
+    const uint32_t b_off_base = MUL == MUL_DIRECT_EXACT ? 0x3F800000u : 0u;
     const float *dummy = reinterpret_cast<const float *>(p.lut);  // valid global address for 0-byte copies
 
     struct Tile {
@@ -473,8 +528,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             uint32_t *d = dec + (g & 1) * Cf::DEC;
             uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + 2 * BK * BM, *b_off = b_al + BK * BN;
             uint32_t amin = 255, amax = 0, bmin = 255, bmax = 0;
-            decode_operand<NT, BM>(ra, p.da.kcontig, a_al, a_off, shift, mask, m + ebytes_log2, lut_base, amin, amax);
-            decode_operand<NT, BN>(rb, p.db.kcontig, b_al, b_off, shift, mask, ebytes_log2, 0u, bmin, bmax);
+            decode_operand<NT, BM, MUL == MUL_NATIVE>(ra, p.da.kcontig, a_al, a_off, shift, mask, a_off_shift,
+                                                      a_off_base, amin, amax);
+            decode_operand<NT, BN, MUL == MUL_NATIVE>(rb, p.db.kcontig, b_al, b_off, shift, mask, b_off_shift,
+                                                      b_off_base, bmin, bmax);
             amin = __reduce_min_sync(0xffffffffu, amin);
             amax = __reduce_max_sync(0xffffffffu, amax);
             bmin = __reduce_min_sync(0xffffffffu, bmin);
@@ -501,7 +558,29 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 
             const uint32_t *A_al = a_al + warp * TM, *A_off = a_off + warp * TM;
             const uint32_t *B_al = b_al + lane * TN, *B_off = b_off + lane * TN;
-            if (fast) {
+            if constexpr (MUL == MUL_NATIVE) {
+                // native FP32 multiply-add of the untruncated operands (IEEE, no FTZ)
+#pragma unroll 2
+                for (int kk = 0; kk < BK; kk++) {
+                    float av[TM], bv[TN];
+#pragma unroll
+                    for (int r = 0; r < TM; r += 4) {
+                        float4 v = *reinterpret_cast<const float4 *>(A_al + kk * BM + r);
+                        av[r] = v.x; av[r + 1] = v.y; av[r + 2] = v.z; av[r + 3] = v.w;
+                    }
+                    if constexpr (TN == 4) {
+                        float4 v = *reinterpret_cast<const float4 *>(B_al + kk * BN);
+                        bv[0] = v.x; bv[1] = v.y; bv[2] = v.z; bv[3] = v.w;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < TN; c++) bv[c] = __uint_as_float(B_al[kk * BN + c]);
+                    }
+#pragma unroll
+                    for (int r = 0; r < TM; r++)
+#pragma unroll
+                        for (int c = 0; c < TN; c++) acc[r][c] = __fmaf_rn(av[r], bv[c], acc[r][c]);
+                }
+            } else if (fast) {
 #pragma unroll 2
                 for (int kk = 0; kk < BK; kk++) {
                     uint32_t aal[TM], aof[TM], bal[TN], bof[TN], mul[TN];
@@ -535,7 +614,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     for (int r = 0; r < TM; r++)
 #pragma unroll
                         for (int c = 0; c < TN; c++) {
-                            uint32_t e = lds_entry<EB>(aof[r] + bof[c]);
+                            uint32_t e = MUL == MUL_LUT ? lut_entry<EB, GL>(aof[r] + bof[c], lut_g)
+                                                        : direct_entry<MUL>(aof[r], bof[c]);
                             uint32_t x = e * mul[c] + bal[c];
                             acc[r][c] = fma_ftz(__uint_as_float(x), __uint_as_float(aal[r]), acc[r][c]);
                         }
@@ -551,7 +631,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                         for (int c = 0; c < TN; c++) {
                             uint32_t bal = B_al[kk * BN + c], bof = B_off[kk * BN + c];
                             uint32_t eb = (bal >> 23) & 0xFFu;
-                            uint32_t ent = lds_entry<EB>(aof + bof) * MULV;  // (carry << 23) | mantissa
+                            uint32_t ent = (MUL == MUL_LUT ? lut_entry<EB, GL>(aof + bof, lut_g)
+                                                           : direct_entry<MUL>(aof, bof)) * MULV;  // (carry << 23) | mantissa
                             uint32_t sgn = (aal ^ bal) & 0x80000000u;
                             int Exp = int(ea + eb) - 127;
                             uint32_t pbits;

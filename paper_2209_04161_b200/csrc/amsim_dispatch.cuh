@@ -1,6 +1,7 @@
-// libamsim: kernel dispatch and the C-ABI compute entry points (include/amsim.h).
-// The device code is in amsim_device.cuh.  Citations "PAPER.md:L" are lines of
-// /root/reference/PAPER.md.
+// libamsim dispatch shared by the per-entry-point translation units
+// (amsim_gemm.cu, amsim_conv_*.cu, amsim_bench.cu): tile configurations,
+// the tile planner and the launch helpers.  Internal; not part of the ABI.
+#pragma once
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,7 +29,7 @@
 namespace amsim {
 namespace dev {
 
-__global__ void fill_zero_kernel(float *C, int M, int N, int64_t ldc)
+static __global__ void fill_zero_kernel(float *C, int M, int N, int64_t ldc)
 {
     int64_t total = int64_t(M) * N;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x)
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(BENCH_NT, 1) lut_bench_kernel(const void *lut,
             const uint32_t aof = ((row[r] + uint32_t(it)) & rmask) << (m + ebl);  // warp-uniform row walk
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                uint32_t e = lds_entry<EB>(aof + bof[c]);
+                uint32_t e = lut_entry<EB>(aof + bof[c], nullptr);
                 acc[r][c] = fma_ftz(__uint_as_float(e * (EB == 8 ? 65536u : 256u) + 0x3F800000u), 1.0f, acc[r][c]);
             }
         }
@@ -220,30 +221,39 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     int mbits = 0;
     amsim_lut_info(lut, &mbits, nullptr);
     uint32_t bytes = uint32_t((size_t(1) << (2 * mbits)) * (eb / 8));
-    if (CfgLean::smem_bytes(bytes) > kSmemMax)
-        return set_error(AMSIM_ERR_UNSUPPORTED, "table of m = " + std::to_string(mbits) + " with " +
-                                                    std::to_string(eb) +
-                                                    "-bit entries does not fit in shared memory (global-memory table: "
-                                                    "future work)");
+    // Tables too large for shared memory (m >= 8 with 32-bit entries, m >= 9)
+    // are read from global memory, where they stay L2-resident (<= 16 MB).
+    p.lut_global = CfgLean::smem_bytes(bytes) > kSmemMax ? 1 : 0;
+    p.mul = MUL_LUT;
+    if (multiply_mode() == AMSIM_MUL_NATIVE) {
+        p.mul = MUL_NATIVE;
+    } else if (multiply_mode() == AMSIM_MUL_DIRECT) {
+        if (lut->model_id < 0)
+            return set_error(AMSIM_ERR_UNSUPPORTED, "AMSIM_MUL_DIRECT needs a table built from a built-in model");
+        p.mul = MUL_DIRECT_EXACT + lut->model_id;
+    }
+    if (p.mul != MUL_LUT) p.lut_global = 0;
     p.lut = tab;
     p.m_bits = mbits;
     p.lut_bytes = bytes;
     p.policy = path_policy() & 1;
     int Mmax = 0;
     for (int i = 0; i < pr.nsub; i++) Mmax = std::max(Mmax, pr.M[i]);
-    p.cfg = int(cfg_for(Mmax, pr.N, bytes));
+    const uint32_t smem_lut = (p.lut_global || p.mul != MUL_LUT) ? 0u : bytes;
+    p.cfg = (p.lut_global || p.mul != MUL_LUT) ? int(pr.N <= 64 ? CfgId::Lean : CfgId::Big)
+                                               : int(cfg_for(Mmax, pr.N, bytes));
     int BM, BN, NT;
     size_t smem;
-    cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, bytes);
+    cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, smem_lut);
     tile_plan(p, pr, BM, BN);
     return AMSIM_OK;
 }
 
-template <class Cf, int EB, class OpA, class OpB>
+template <class Cf, int EB, class OpA, class OpB, bool GL = false, int MUL = MUL_LUT>
 static amsim_status launch_cfg(const KParams &p, const OpA &a, const OpB &b, cudaStream_t st)
 {
-    size_t smem = Cf::smem_bytes(p.lut_bytes);
-    auto kern = amsim_mm_kernel<Cf, EB, OpA, OpB>;
+    size_t smem = Cf::smem_bytes((GL || MUL != MUL_LUT) ? 0u : p.lut_bytes);
+    auto kern = amsim_mm_kernel<Cf, EB, OpA, OpB, GL, MUL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
     int grid = std::min(p.ntiles, num_sms());
@@ -253,9 +263,28 @@ static amsim_status launch_cfg(const KParams &p, const OpA &a, const OpB &b, cud
     return cuda_check(cudaGetLastError(), "amsim_mm_kernel launch");
 }
 
+template <int MUL, class OpA, class OpB>
+static amsim_status launch_mode(const KParams &p, const OpA &a, const OpB &b, cudaStream_t st)
+{
+    return CfgId(p.cfg) == CfgId::Lean ? launch_cfg<CfgLean, 32, OpA, OpB, false, MUL>(p, a, b, st)
+                                       : launch_cfg<CfgBig, 32, OpA, OpB, false, MUL>(p, a, b, st);
+}
+
 template <int EB, class OpA, class OpB>
 static amsim_status launch_eb(const KParams &p, const OpA &a, const OpB &b, cudaStream_t st)
 {
+    switch (p.mul) {
+    case MUL_NATIVE: return launch_mode<MUL_NATIVE>(p, a, b, st);
+    case MUL_DIRECT_EXACT: return launch_mode<MUL_DIRECT_EXACT>(p, a, b, st);
+    case MUL_DIRECT_MITCHELL: return launch_mode<MUL_DIRECT_MITCHELL>(p, a, b, st);
+    case MUL_DIRECT_MBM: return launch_mode<MUL_DIRECT_MBM>(p, a, b, st);
+    default: break;
+    }
+    if (p.lut_global) {
+        if constexpr (EB == 8) return set_error(AMSIM_ERR_UNSUPPORTED, "8-bit tables always fit shared memory");
+        else return CfgId(p.cfg) == CfgId::Lean ? launch_cfg<CfgLean, EB, OpA, OpB, true>(p, a, b, st)
+                                                 : launch_cfg<CfgBig, EB, OpA, OpB, true>(p, a, b, st);
+    }
     switch (CfgId(p.cfg)) {
     case CfgId::Small: return launch_cfg<CfgSmall, EB>(p, a, b, st);
     case CfgId::Mid: return launch_cfg<CfgMid, EB>(p, a, b, st);
@@ -282,7 +311,9 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
         }
         p.ws = ws;
     }
-    amsim_status s = eb == 8 ? launch_eb<8>(p, a, b, st) : (eb == 16 ? launch_eb<16>(p, a, b, st) : launch_eb<32>(p, a, b, st));
+    amsim_status s = (eb == 8 && p.mul == MUL_LUT)    ? launch_eb<8>(p, a, b, st)
+                     : (eb == 16 && p.mul == MUL_LUT) ? launch_eb<16>(p, a, b, st)
+                                                      : launch_eb<32>(p, a, b, st);
     if (s == AMSIM_OK && p.ws_elems > 0) {
         int64_t maxmn = 0;
         for (int i = 0; i < p.nsub; i++) maxmn = std::max<int64_t>(maxmn, int64_t(p.sub[i].M) * p.N);
@@ -353,239 +384,3 @@ static void dgrad_phases(const amsim_conv2d_desc *d, Problem &pr, DgPhase *ph)
 }
 
 }  // namespace amsim
-
-using namespace amsim;
-
-extern "C" {
-
-amsim_status amsim_gemm(const amsim_lut *lut, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
-                        const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc,
-                        int accumulate, amsim_stream_t stream)
-{
-    clear_error();
-    if (!lut) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_gemm: null lut");
-    if (M < 0 || N < 0 || K < 0) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_gemm: negative size");
-    if (M >= (1LL << 31) || N >= (1LL << 31) || K >= (1LL << 31))
-        return set_error(AMSIM_ERR_INVALID_ARG, "amsim_gemm: dimensions must be < 2^31");
-    if (M == 0 || N == 0) return AMSIM_OK;
-    if (!C || ldc < N) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_gemm: C null or ldc < N");
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (K == 0) {
-        const void *tab;
-        int eb;
-        amsim_status s = device_table(lut, &tab, &eb);  // device check
-        if (s != AMSIM_OK) return s;
-        if (accumulate) return AMSIM_OK;
-        fill_zero_kernel<<<std::max(1, int(std::min<int64_t>((M * N + 255) / 256, 1024))), 256, 0, st>>>(C, int(M),
-                                                                                                         int(N), ldc);
-        count_launch();
-        return cuda_check(cudaGetLastError(), "fill_zero launch");
-    }
-    if (!A || !B) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_gemm: null operand");
-    if ((!trans_a && lda < K) || (trans_a && lda < M))
-        return set_error(AMSIM_ERR_INVALID_ARG, "amsim_gemm: lda too small");
-    if ((!trans_b && ldb < N) || (trans_b && ldb < K))
-        return set_error(AMSIM_ERR_INVALID_ARG, "amsim_gemm: ldb too small");
-    Problem pr;
-    pr.N = int(N);
-    pr.M[0] = int(M);
-    pr.K[0] = int(K);
-    KParams p{};
-    int eb = 32;
-    amsim_status s = prepare(lut, p, pr, eb);
-    if (s != AMSIM_OK) return s;
-    GemmOp a{A, lda, int(M), int(K), trans_a ? 0 : 1};
-    GemmOp b{B, ldb, int(N), int(K), trans_b ? 1 : 0};
-    // 16-byte copies need 4 contiguous elements with 16-B aligned rows
-    bool va = aligned16(A) && lda % 4 == 0 && (trans_a ? M % 4 == 0 : K % 4 == 0);
-    bool vb = aligned16(B) && ldb % 4 == 0 && (trans_b ? K % 4 == 0 : N % 4 == 0);
-    p.da = OpDesc{a.kcontig, va ? 2 : 0};
-    p.db = OpDesc{b.kcontig, vb ? 2 : 0};
-    p.C = C;
-    p.ldc = ldc;
-    p.accumulate = accumulate;
-    return run(eb, p, a, b, st);
-}
-
-amsim_status amsim_conv2d_fwd(const amsim_lut *lut, const amsim_conv2d_desc *d, const float *x, const float *w,
-                              float *y, amsim_stream_t stream)
-{
-    clear_error();
-    if (!lut) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_fwd: null lut");
-    amsim_status s = check_desc(d);
-    if (s != AMSIM_OK) return s;
-    if (d->N == 0) return AMSIM_OK;
-    if (!x || !w || !y) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_fwd: null tensor");
-    ConvGeom g;
-    init_geom(g, d);
-    Problem pr;
-    pr.N = d->K;
-    pr.M[0] = d->N * g.OH * g.OW;
-    pr.K[0] = d->R * d->S * d->C;
-    KParams p{};
-    int eb = 32;
-    s = prepare(lut, p, pr, eb);
-    if (s != AMSIM_OK) return s;
-    FwdX a{x, g, pr.M[0], pr.K[0]};
-    GemmOp b{w, pr.N, pr.N, pr.K[0], 0};
-    p.da = OpDesc{1, (d->C % 4 == 0 && aligned16(x)) ? 2 : 0};
-    p.db = OpDesc{0, (pr.N % 4 == 0 && aligned16(w)) ? 2 : 0};
-    p.C = y;
-    p.ldc = pr.N;
-    p.accumulate = 0;
-    return run(eb, p, a, b, reinterpret_cast<cudaStream_t>(stream));
-}
-
-amsim_status amsim_conv2d_bwd_data(const amsim_lut *lut, const amsim_conv2d_desc *d, const float *dy,
-                                   const float *w, float *dx, amsim_stream_t stream)
-{
-    clear_error();
-    if (!lut) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_data: null lut");
-    amsim_status s = check_desc(d);
-    if (s != AMSIM_OK) return s;
-    if (d->N == 0) return AMSIM_OK;
-    if (!dy || !w || !dx) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_data: null tensor");
-    DgDY a{};
-    DgW b{};
-    init_geom(a.g, d);
-    Problem pr;
-    dgrad_phases(d, pr, a.ph);
-    a.dy = dy;
-    a.fK.init(uint32_t(d->K));
-    b.w = w;
-    b.g = a.g;
-    b.fK = a.fK;
-    std::memcpy(b.ph, a.ph, sizeof(a.ph));
-    KParams p{};
-    int eb = 32;
-    s = prepare(lut, p, pr, eb);
-    if (s != AMSIM_OK) return s;
-    bool v = d->K % 4 == 0;
-    p.da = OpDesc{1, (v && aligned16(dy)) ? 2 : 0};
-    p.db = OpDesc{1, (v && aligned16(w)) ? 2 : 0};
-    p.C = dx;
-    p.ldc = d->C;
-    p.accumulate = 0;
-    return run(eb, p, a, b, reinterpret_cast<cudaStream_t>(stream));
-}
-
-static amsim_status wgrad_plan(const amsim_lut *lut, const amsim_conv2d_desc *d, KParams &p, ConvGeom &g, int &eb)
-{
-    init_geom(g, d);
-    Problem pr;
-    pr.N = d->K;
-    pr.M[0] = d->R * d->S * d->C;
-    pr.K[0] = d->N * g.OH * g.OW;
-    pr.max_splits = 1024;
-    return prepare(lut, p, pr, eb);
-}
-
-amsim_status amsim_conv2d_bwd_filter_workspace(const amsim_lut *lut, const amsim_conv2d_desc *d, size_t *bytes)
-{
-    clear_error();
-    if (!lut || !bytes) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter_workspace: null argument");
-    amsim_status s = check_desc(d);
-    if (s != AMSIM_OK) return s;
-    KParams p{};
-    ConvGeom g;
-    int eb;
-    s = wgrad_plan(lut, d, p, g, eb);
-    if (s != AMSIM_OK) return s;
-    *bytes = size_t(p.ws_elems) * sizeof(float);
-    return AMSIM_OK;
-}
-
-amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_desc *d, const float *x,
-                                     const float *dy, float *dw, void *workspace, size_t workspace_bytes,
-                                     amsim_stream_t stream)
-{
-    clear_error();
-    if (!lut) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter: null lut");
-    amsim_status s = check_desc(d);
-    if (s != AMSIM_OK) return s;
-    if (!x || !dy || !dw) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter: null tensor");
-    KParams p{};
-    ConvGeom g;
-    int eb;
-    s = wgrad_plan(lut, d, p, g, eb);
-    if (s != AMSIM_OK) return s;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const SubP &S = p.sub[0];
-    if (S.K == 0) {
-        fill_zero_kernel<<<64, 256, 0, st>>>(dw, S.M, p.N, p.N);
-        count_launch();
-        return cuda_check(cudaGetLastError(), "fill_zero launch");
-    }
-    size_t need = size_t(p.ws_elems) * sizeof(float);
-    if (need > 0 && (!workspace || workspace_bytes < need))
-        return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter: workspace too small (need " +
-                                                    std::to_string(need) + " bytes)");
-    WgX a{x, g, S.M, S.K};
-    GemmOp b{dy, d->K, p.N, S.K, 0};
-    p.da = OpDesc{0, (d->C % 4 == 0 && aligned16(x)) ? 2 : 0};
-    p.db = OpDesc{0, (d->K % 4 == 0 && aligned16(dy)) ? 2 : 0};
-    p.C = dw;
-    p.ldc = p.N;
-    p.accumulate = 0;
-    return run(eb, p, a, b, st, static_cast<float *>(workspace));
-}
-
-amsim_status amsim_bench_lut_lookup(int m_bits, int entry_bits, int iters, const uint32_t *b_idx_host, size_t n_idx,
-                                    double *lookups_per_s, amsim_stream_t stream)
-{
-    clear_error();
-    if (m_bits < 1 || m_bits > 8 || (entry_bits != 8 && entry_bits != 16 && entry_bits != 32) || iters <= 0 ||
-        !b_idx_host || !n_idx ||
-        !lookups_per_s)
-        return set_error(AMSIM_ERR_INVALID_ARG, "amsim_bench_lut_lookup: bad argument");
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    uint32_t bytes = uint32_t((size_t(1) << (2 * m_bits)) * (entry_bits / 8));
-    if (bytes > 200 * 1024) return set_error(AMSIM_ERR_UNSUPPORTED, "table too large for shared memory");
-    void *tab = nullptr;
-    uint32_t *idx = nullptr;
-    float *out = nullptr;
-    int sms = num_sms();
-    amsim_status s = AMSIM_OK;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    do {
-        if ((s = cuda_check(cudaMalloc(&tab, bytes), "cudaMalloc")) != AMSIM_OK) break;
-        if ((s = cuda_check(cudaMemsetAsync(tab, 0, bytes, st), "memset")) != AMSIM_OK) break;
-        if ((s = cuda_check(cudaMalloc(&idx, n_idx * 4), "cudaMalloc")) != AMSIM_OK) break;
-        if ((s = cuda_check(cudaMemcpyAsync(idx, b_idx_host, n_idx * 4, cudaMemcpyHostToDevice, st), "memcpy")) !=
-            AMSIM_OK)
-            break;
-        if ((s = cuda_check(cudaMalloc(&out, size_t(sms) * BENCH_NT * 4), "cudaMalloc")) != AMSIM_OK) break;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        auto launch = [&]() {
-            if (entry_bits == 8) {
-                cudaFuncSetAttribute(lut_bench_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-                lut_bench_kernel<8><<<sms, BENCH_NT, bytes, st>>>(tab, bytes, m_bits, idx, int(n_idx), iters, out);
-            } else if (entry_bits == 16) {
-                cudaFuncSetAttribute(lut_bench_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-                lut_bench_kernel<16><<<sms, BENCH_NT, bytes, st>>>(tab, bytes, m_bits, idx, int(n_idx), iters, out);
-            } else {
-                cudaFuncSetAttribute(lut_bench_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-                lut_bench_kernel<32><<<sms, BENCH_NT, bytes, st>>>(tab, bytes, m_bits, idx, int(n_idx), iters, out);
-            }
-            count_launch();
-        };
-        launch();  // warm-up
-        cudaEventRecord(e0, st);
-        launch();
-        cudaEventRecord(e1, st);
-        if ((s = cuda_check(cudaEventSynchronize(e1), "bench sync")) != AMSIM_OK) break;
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e1);
-        double lookups = double(sms) * BENCH_NT * iters * BENCH_TM * 4;
-        *lookups_per_s = lookups / (ms * 1e-3);
-    } while (0);
-    if (e0) cudaEventDestroy(e0);
-    if (e1) cudaEventDestroy(e1);
-    cudaFree(tab);
-    cudaFree(idx);
-    cudaFree(out);
-    return s;
-}
-
-}  // extern "C"

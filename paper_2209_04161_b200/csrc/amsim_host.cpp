@@ -16,6 +16,7 @@ namespace amsim {
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int> g_policy{0};
+static std::atomic<int> g_mul_mode{0};
 
 amsim_status set_error(amsim_status s, const std::string &msg)
 {
@@ -28,6 +29,8 @@ void clear_error() { g_last_error.clear(); }
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int path_policy() { return g_policy.load(std::memory_order_relaxed); }
+
+int multiply_mode() { return g_mul_mode.load(std::memory_order_relaxed); }
 
 static inline uint32_t bits(float f)
 {
@@ -133,6 +136,14 @@ amsim_status amsim_set_path_policy(int policy)
     return AMSIM_OK;
 }
 
+amsim_status amsim_set_multiply_mode(int mode)
+{
+    if (mode < AMSIM_MUL_LUT || mode > AMSIM_MUL_DIRECT)
+        return set_error(AMSIM_ERR_INVALID_ARG, "multiply mode must be AMSIM_MUL_LUT, _NATIVE or _DIRECT");
+    g_mul_mode.store(mode);
+    return AMSIM_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Built-in functional models (integer fixed point on the 23-bit fraction).
 
@@ -192,6 +203,7 @@ amsim_status amsim_lut_build(amsim_mul_fn model, int m, amsim_lut **out)
     amsim_lut *lut = new (std::nothrow) amsim_lut;
     if (!lut) return set_error(AMSIM_ERR_NOMEM, "amsim_lut_build: out of host memory");
     lut->m = m;
+    lut->model_id = model == amsim_model_exact ? 0 : model == amsim_model_mitchell ? 1 : model == amsim_model_mbm ? 2 : -1;
     const uint32_t n = 1u << m;
     try {
         lut->entries.resize(size_t(n) * n);

@@ -1,5 +1,5 @@
 // Internal declarations shared by the host side (amsim_host.cpp) and the
-// kernel side (amsim_kernels.cu) of libamsim.  Not part of the ABI.
+// kernel side (amsim_dispatch.cuh and the amsim_*.cu entry points) of libamsim.  Not part of the ABI.
 #pragma once
 
 #include <cstdint>
@@ -27,6 +27,7 @@ struct DeviceTable {
 struct amsim_lut {
     int m = 0;
     std::vector<uint32_t> entries;   // Alg. 1 layout: (carry << 23) | mantissa
+    int model_id = -1;               // built-in model the table was built from (0 exact, 1 Mitchell, 2 MBM), else -1
     int device_entry_bits = 32;      // 8 if every (e & 0xFFFF) == 0, else 16 if every (e & 0xFF) == 0
     std::mutex mu;
     amsim::DeviceTable dev[amsim::kMaxDevices];        // narrowest layout
@@ -45,5 +46,6 @@ amsim_status device_table(const amsim_lut *lut, const void **ptr, int *entry_bit
 void count_launch(uint64_t n = 1);
 
 int path_policy();
+int multiply_mode();
 
 }  // namespace amsim

@@ -108,6 +108,53 @@ def test_k1_outer_product_exhaustive(am, luts, orc, model, m, policy):
     assert_bits(got, want, f"{model} m={m} policy={policy}")
 
 
+def _sampled_grid(m, n_mant=96, seed=5):
+    """operand_grid restricted to a sample of the 2^m mantissas (the first and
+    last four always included) -- the exhaustive grid is too large for m >= 9."""
+    v = inp.operand_grid(m).view(np.uint32)
+    mant = (v >> np.uint32(23 - m)) & np.uint32((1 << m) - 1)
+    keep = np.unique(np.concatenate([np.arange(4), (1 << m) - 1 - np.arange(4),
+                                     inp.rng(seed).integers(0, 1 << m, n_mant)]))
+    normal = ((v >> 23) & 0xFF) != 0
+    normal &= ((v >> 23) & 0xFF) != 0xFF
+    sel = ~normal | np.isin(mant, keep)
+    return v[sel].view(np.float32)
+
+
+@pytest.mark.parametrize("model,m,width", [("exact", 8, 32), ("exact", 11, 32), ("mitchell", 9, 16),
+                                           ("mitchell", 11, 16), ("mbm", 10, 16)])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_k1_outer_product_global_table(am, luts, orc, model, m, width, policy):
+    """Tables too large for shared memory (m >= 8 with 32-bit entries, m >= 9)
+    are read from global memory / L2; per-product bits are unchanged."""
+    lut = luts(model, m)
+    assert lut.info() == (m, width)
+    v = _sampled_grid(m)
+    am.amsim_set_path_policy(policy)
+    try:
+        got = run_gemm(am, lut, v[:, None], v[None, :])
+    finally:
+        am.amsim_set_path_policy(0)
+    assert_bits(got, orc.mul(v[:, None], v[None, :], model, m), f"{model} m={m} policy={policy}")
+
+
+@pytest.mark.parametrize("model,m", [("mitchell", 9), ("exact", 8)])
+def test_global_table_gemm_and_conv(am, luts, orc, model, m):
+    lut = luts(model, m)
+    A = inp.normal((130, 77), 81)
+    B = inp.normal((77, 200), 82)
+    shape = (2, 14, 14, 16, 72, 3, 3, 2, 1)
+    x, w, dy, OH, OW = _conv_tensors(shape, 83)
+    d = am.conv_desc(*shape)
+    od = orc.conv_desc(*shape)
+    with exact_order(am):
+        assert_bits(run_gemm(am, lut, A, B), orc.gemm(A, B, model, m).c32, "gemm")
+        assert_bits(_run_conv(am, lut, d, x, w, dy, "fwd"), orc.conv_fwd(od, x, w, model, m).c32, "fwd")
+        assert_bits(_run_conv(am, lut, d, x, w, dy, "dgrad"), orc.conv_bwd_data(od, dy, w, model, m).c32, "dgrad")
+        assert_bits(_run_conv(am, lut, d, x, w, dy, "wgrad"), orc.conv_bwd_filter(od, x, dy, model, m).c32, "wgrad")
+    assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), orc.conv_bwd_filter(od, x, dy, model, m), "wgrad split")
+
+
 @pytest.mark.parametrize("model", ["exact", "mitchell", "mbm"])
 def test_fast_path_full_exponent_range(am, luts, orc, model):
     """Operands whose exponent ranges keep every Exp in [1, 253] take the FTZ
@@ -296,7 +343,8 @@ def test_conv_vs_oracle(am, luts, orc, shape, which, model):
     assert_bits(got, res.c32, f"{which} {shape} vs c32")
 
 
-@pytest.mark.parametrize("model,m,width", [("mitchell", 7, 8), ("exact", 3, 8), ("mbm", 7, 16), ("exact", 6, 16)])
+@pytest.mark.parametrize("model,m,width", [("mitchell", 7, 8), ("exact", 3, 8), ("mbm", 7, 16), ("exact", 6, 16),
+                                             ("mitchell", 8, 16)])
 def test_entry_layout_never_changes_bits(am, luts, orc, model, m, width):
     """The narrow device layouts (8-bit: carry | 7 mantissa bits; 16-bit) give
     the same bits as the 32-bit Alg. 1 layout (policy bit 2), for GEMM and all
@@ -466,3 +514,63 @@ def test_train_step_lenet(am, luts):
     am.amsim_conv2d_bwd_filter(lut, ly.desc, ly.x, ly.dy, dw, ws)
     torch.cuda.synchronize()
     assert torch.equal(dw, ly.dw)
+
+
+# ---------------------------------------------------------------------------
+# measurement instruments: direct model evaluation (no table) and native multiply
+
+@pytest.mark.parametrize("model,m", [("exact", 7), ("mitchell", 7), ("mbm", 7), ("exact", 11), ("mitchell", 4),
+                                     ("mbm", 10), ("exact", 1)])
+def test_direct_mode_equals_table(am, luts, orc, model, m):
+    """AMSIM_MUL_DIRECT evaluates the built-in model per product on the device
+    (the paper's "direct simulation") -- same bits as the
+    table and the oracle, on the special-value grid (fast and careful paths)."""
+    lut = luts(model, m)
+    v = _sampled_grid(m) if m > 7 else inp.operand_grid(m)
+    want = orc.mul(v[:, None], v[None, :], model, m)
+    for policy in (0, 1):
+        am.amsim_set_path_policy(policy)
+        try:
+            with am.multiply_mode(am.AMSIM_MUL_DIRECT):
+                got = run_gemm(am, lut, v[:, None], v[None, :])
+        finally:
+            am.amsim_set_path_policy(0)
+        assert_bits(got, want, f"direct {model} m={m} policy={policy}")
+
+
+@pytest.mark.parametrize("model", ["exact", "mitchell", "mbm"])
+def test_direct_mode_conv_equals_table(am, luts, model):
+    lut = luts(model)
+    shape = (2, 14, 14, 16, 72, 3, 3, 2, 1)
+    x, w, dy, OH, OW = _conv_tensors(shape, 91)
+    d = am.conv_desc(*shape)
+    for which in ("fwd", "dgrad", "wgrad"):
+        ref = _run_conv(am, lut, d, x, w, dy, which)
+        with am.multiply_mode(am.AMSIM_MUL_DIRECT):
+            got = _run_conv(am, lut, d, x, w, dy, which)
+        assert_bits(got, ref, f"{model} {which}")
+
+
+def test_direct_mode_needs_builtin_model(am, luts):
+    import torch
+    lut = am.Lut.from_entries(luts("exact", 4).entries(), 4)
+    C = torch.empty((2, 2), device="cuda")
+    with am.multiply_mode(am.AMSIM_MUL_DIRECT):
+        with pytest.raises(am.AmsimError):
+            am.amsim_gemm(lut, torch.ones((2, 3), device="cuda"), torch.ones((3, 2), device="cuda"), C)
+
+
+def test_native_mode_is_fp32_gemm(am, luts):
+    """AMSIM_MUL_NATIVE (the ATnG analog): IEEE FP32 products of the
+    UNtruncated operands, fma-accumulated from +0 in increasing k."""
+    A = inp.normal((130, 300), 95)
+    B = inp.normal((300, 70), 96)
+    with exact_order(am), am.multiply_mode(am.AMSIM_MUL_NATIVE):
+        got = run_gemm(am, luts("mbm"), A, B)
+    want = np.zeros((130, 70), np.float32)
+    for k in range(300):                       # sequential fp32 fma order
+        want = (want.astype(np.float64) + A[:, k:k + 1].astype(np.float64) * B[k:k + 1, :]).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    absum = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64)
+    assert np.all(np.abs(got - ref) <= 1e-5 * absum)
+    assert np.max(np.abs(got.astype(np.float64) - want)) <= 1e-6 * absum.max()

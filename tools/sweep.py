@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--models", nargs="+", default=["mitchell", "exact"])
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--policy", type=int, default=0)
+    ap.add_argument("--modes", nargs="+", default=["lut"], choices=["lut", "native", "direct"],
+                    help="multiply mode: the AMSim table (product) or the native / direct-model instruments")
     args = ap.parse_args()
 
     import numpy as np
@@ -41,9 +43,13 @@ def main():
             width = lut.info()[1]
             if (m, width) not in idx_cache:
                 idx = np.random.default_rng(0).integers(0, 1 << m, 1 << 16).astype(np.uint32)
-                idx_cache[(m, width)] = am.amsim_bench_lut_lookup(m, width, idx, iters=2048) / 1e9
+                try:
+                    idx_cache[(m, width)] = am.amsim_bench_lut_lookup(m, width, idx, iters=2048) / 1e9
+                except am.AmsimError:       # table beyond shared memory: no smem-lookup instrument
+                    idx_cache[(m, width)] = None
             lookup = idx_cache[(m, width)]
-            for n in args.sizes:
+            for n, mode in [(n, md) for n in args.sizes for md in args.modes]:
+                am.amsim_set_multiply_mode({"lut": 0, "native": 1, "direct": 2}[mode])
                 A = gen.normal((n, n), 1, device=dev)
                 B = gen.normal((n, n), 2, device=dev)
                 C = torch.empty((n, n), device=dev)
@@ -59,9 +65,11 @@ def main():
                 ms = ev[0].elapsed_time(ev[1]) / reps
                 gmacs = n ** 3 / (ms * 1e-3) / 1e9
                 peak = sms * 32 * 1965e6 / 1e9
-                print(json.dumps({"model": model, "m": m, "entry_bits": width, "M": n, "N": n, "K": n,
+                am.amsim_set_multiply_mode(0)
+                print(json.dumps({"mode": mode, "model": model, "m": m, "entry_bits": width, "M": n, "N": n, "K": n,
                                   "ms": ms, "gmacs": gmacs, "frac_of_32_lookups_per_clk": gmacs / peak,
-                                  "lookup_measured_gps": lookup, "frac_of_measured_lookup": gmacs / lookup,
+                                  "lookup_measured_gps": lookup,
+                                  "frac_of_measured_lookup": gmacs / lookup if lookup else None,
                                   "reps": reps}), flush=True)
                 del A, B, C
                 torch.cuda.empty_cache()
