@@ -312,6 +312,18 @@ def main():
             cpu = {"value": None, "unit": "GMAC/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {ex}"}
 
+    # DRAM traffic of the dominant kernel kind per layer pass, from the committed
+    # ncu launch list of this same command (profiles/; tools/summarize_launches.py)
+    traffic, traffic_note = None, None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if args.workload == "resnet50" and os.path.exists(tpath):
+        t = json.load(open(tpath)).get(dom_kind)
+        if t:
+            traffic = t["dram_bytes_per_pass"]
+            traffic_note = (f"ncu dram bytes per {dom_kind} pass (avg over {t['layer_passes']} passes) from "
+                            f"profiles/r01_traffic.json; algorithmic 4(|X|+|W|+|Y|) = "
+                            f"{t['algorithmic_bytes_per_pass']:.4g} B/pass (ratio {t['ratio']:.3f})")
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,
@@ -326,7 +338,9 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": {"bound": "alu", "kernel": f"amsim_mm_kernel [{dom_kind}]", "achieved": achieved,
-                         "peak": peak, "unit": "GMAC/s", "frac": achieved / peak, "traffic": None,
+                         "peak": peak, "unit": "GMAC/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_note": traffic_note,
+                         "frac_of_measured_lookup": (achieved / lut_meas) if isinstance(lut_meas, float) else None,
                          "peak_basis": "148 SMs x 32 LUT lookups/clk (conflict-free LDS = 4-instr/MAC issue "
                                        "ceiling) x max SM clock",
                          "lut_lookup_measured_gps": lut_meas,

@@ -7,7 +7,8 @@ using namespace amsim::dev;
 
 extern "C" {
 
-static amsim_status wgrad_plan(const amsim_lut *lut, const amsim_conv2d_desc *d, KParams &p, ConvGeom &g, int &eb)
+static amsim_status wgrad_plan(const amsim_lut *lut, const amsim_conv2d_desc *d, KParams &p, ConvGeom &g, int &eb,
+                               int mode = -1, int policy = -1)
 {
     init_geom(g, d);
     Problem pr;
@@ -15,7 +16,7 @@ static amsim_status wgrad_plan(const amsim_lut *lut, const amsim_conv2d_desc *d,
     pr.M[0] = d->R * d->S * d->C;
     pr.K[0] = d->N * g.OH * g.OW;
     pr.max_splits = 1024;
-    return prepare(lut, p, pr, eb);
+    return prepare(lut, p, pr, eb, mode, policy);
 }
 
 amsim_status amsim_conv2d_bwd_filter_workspace(const amsim_lut *lut, const amsim_conv2d_desc *d, size_t *bytes)
@@ -24,12 +25,20 @@ amsim_status amsim_conv2d_bwd_filter_workspace(const amsim_lut *lut, const amsim
     if (!lut || !bytes) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter_workspace: null argument");
     amsim_status s = check_desc(d);
     if (s != AMSIM_OK) return s;
-    KParams p{};
-    ConvGeom g;
-    int eb;
-    s = wgrad_plan(lut, d, p, g, eb);
-    if (s != AMSIM_OK) return s;
-    *bytes = size_t(p.ws_elems) * sizeof(float);
+    // The plan (hence the workspace) depends on the multiply mode and the
+    // table layout policy; report the maximum so one allocation serves all.
+    int64_t need = 0;
+    const int pol = path_policy() & 3;
+    for (int mode : {AMSIM_MUL_LUT, AMSIM_MUL_NATIVE})
+        for (int policy : {pol, pol | 4}) {
+            KParams p{};
+            ConvGeom g;
+            int eb;
+            s = wgrad_plan(lut, d, p, g, eb, mode, policy);
+            if (s != AMSIM_OK) return s;
+            need = std::max<int64_t>(need, p.ws_elems);
+        }
+    *bytes = size_t(need) * sizeof(float);
     return AMSIM_OK;
 }
 

@@ -302,6 +302,10 @@ struct KCfg {
     static constexpr int TN = TN_;
     static constexpr int BM = NWARPS * TM;
     static constexpr int BN = 32 * TN;
+    // a lane owns columns lane * CG + col(c), c < TN: groups of 4 consecutive
+    // columns 128 apart when TN >= 4 (conflict-free LDS.128), else TN consecutive
+    static constexpr int CG = TN >= 4 ? 4 : TN;
+    static constexpr __host__ __device__ int col(int c) { return TN >= 4 ? (c >> 2) * 128 + (c & 3) : c; }
     static constexpr int RAW_A = BM * (BK + RAW_PAD);
     static constexpr int RAW_B = BN * (BK + RAW_PAD);
     static constexpr int RAW_STAGE = RAW_A + RAW_B;        // floats
@@ -417,6 +421,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                                                              const __grid_constant__ OpB opb)
 {
     constexpr int NT = Cf::NT, NWARPS = Cf::NWARPS, TM = Cf::TM, TN = Cf::TN, BM = Cf::BM, BN = Cf::BN;
+    constexpr int CG = Cf::CG;
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -557,7 +562,9 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                               (Amax == 0 || Bmax == 0 || (Amin + Bmin >= 128 && Amax + Bmax <= 380));
 
             const uint32_t *A_al = a_al + warp * TM, *A_off = a_off + warp * TM;
-            const uint32_t *B_al = b_al + lane * TN, *B_off = b_off + lane * TN;
+            // lane columns: groups of 4 consecutive columns, group g at g * 128
+            // (TN >= 4: each LDS.128 of a group covers 512 contiguous bytes), else TN consecutive
+            const uint32_t *B_al = b_al + lane * CG, *B_off = b_off + lane * CG;
             if constexpr (MUL == MUL_NATIVE) {
                 // native FP32 multiply-add of the untruncated operands (IEEE, no FTZ)
 #pragma unroll 2
@@ -568,9 +575,12 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                         float4 v = *reinterpret_cast<const float4 *>(A_al + kk * BM + r);
                         av[r] = v.x; av[r + 1] = v.y; av[r + 2] = v.z; av[r + 3] = v.w;
                     }
-                    if constexpr (TN == 4) {
-                        float4 v = *reinterpret_cast<const float4 *>(B_al + kk * BN);
-                        bv[0] = v.x; bv[1] = v.y; bv[2] = v.z; bv[3] = v.w;
+                    if constexpr (TN % 4 == 0) {
+#pragma unroll
+                        for (int c = 0; c < TN; c += 4) {
+                            float4 v = *reinterpret_cast<const float4 *>(B_al + kk * BN + c * 32);
+                            bv[c] = v.x; bv[c + 1] = v.y; bv[c + 2] = v.z; bv[c + 3] = v.w;
+                        }
                     } else {
 #pragma unroll
                         for (int c = 0; c < TN; c++) bv[c] = __uint_as_float(B_al[kk * BN + c]);
@@ -591,11 +601,14 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                         aal[r] = v.x; aal[r + 1] = v.y; aal[r + 2] = v.z; aal[r + 3] = v.w;
                         aof[r] = o.x; aof[r + 1] = o.y; aof[r + 2] = o.z; aof[r + 3] = o.w;
                     }
-                    if constexpr (TN == 4) {
-                        uint4 v = *reinterpret_cast<const uint4 *>(B_al + kk * BN);
-                        uint4 o = *reinterpret_cast<const uint4 *>(B_off + kk * BN);
-                        bal[0] = v.x; bal[1] = v.y; bal[2] = v.z; bal[3] = v.w;
-                        bof[0] = o.x; bof[1] = o.y; bof[2] = o.z; bof[3] = o.w;
+                    if constexpr (TN % 4 == 0) {
+#pragma unroll
+                        for (int c = 0; c < TN; c += 4) {
+                            uint4 v = *reinterpret_cast<const uint4 *>(B_al + kk * BN + c * 32);
+                            uint4 o = *reinterpret_cast<const uint4 *>(B_off + kk * BN + c * 32);
+                            bal[c] = v.x; bal[c + 1] = v.y; bal[c + 2] = v.z; bal[c + 3] = v.w;
+                            bof[c] = o.x; bof[c + 1] = o.y; bof[c + 2] = o.z; bof[c + 3] = o.w;
+                        }
                     } else if constexpr (TN == 2) {
                         uint2 v = *reinterpret_cast<const uint2 *>(B_al + kk * BN);
                         uint2 o = *reinterpret_cast<const uint2 *>(B_off + kk * BN);
@@ -629,7 +642,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                         uint32_t ea = (aal >> 23) & 0xFFu;
 #pragma unroll
                         for (int c = 0; c < TN; c++) {
-                            uint32_t bal = B_al[kk * BN + c], bof = B_off[kk * BN + c];
+                            uint32_t bal = B_al[kk * BN + Cf::col(c)], bof = B_off[kk * BN + Cf::col(c)];
                             uint32_t eb = (bal >> 23) & 0xFFu;
                             uint32_t ent = (MUL == MUL_LUT ? lut_entry<EB, GL>(aof + bof, lut_g)
                                                            : direct_entry<MUL>(aof, bof)) * MULV;  // (carry << 23) | mantissa
@@ -663,7 +676,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             float *dst = Cb + (split_out ? int64_t(row) * p.N : opa.out_row(T.s, row, p.ldc));
 #pragma unroll
             for (int c = 0; c < TN; c++) {
-                int col = T.n0 + lane * TN + c;
+                int col = T.n0 + lane * CG + Cf::col(c);
                 if (col >= p.N) continue;
                 dst[col] = (p.accumulate && !split_out) ? (dst[col] + acc[r][c]) : acc[r][c];
             }

@@ -5,8 +5,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -82,9 +85,13 @@ using namespace dev;
 
 using CfgSmall = KCfg<256, 8, 1>;                        // N <= 32
 using CfgMid = KCfg<AMSIM_NT_MID, AMSIM_TM_MID, 2>;      // N <= 64, M > 64
-using CfgBig = KCfg<AMSIM_NT_BIG, AMSIM_TM_BIG, 4>;      // N > 64, M > 64
+#ifndef AMSIM_TN_BIG
+#define AMSIM_TN_BIG 4
+#endif
+using CfgBig = KCfg<AMSIM_NT_BIG, AMSIM_TM_BIG, AMSIM_TN_BIG>;  // N > 64, M > 64
 using CfgLean = KCfg<256, 8, 2>;                         // N <= 64, M <= 64; and tables too large for the others
 using CfgWide = KCfg<256, 8, 4>;                         // N > 64, M <= 64
+using CfgHuge = KCfg<256, 16, 8>;                        // N >= 256, 16/32-bit tables (fewer operand loads per lookup)
 
 static int g_num_sms = 0;
 static int num_sms()
@@ -113,7 +120,7 @@ struct Problem {
     int max_splits = 64;
 };
 
-enum class CfgId { Small, Mid, Big, Lean, Wide };
+enum class CfgId { Small, Mid, Big, Lean, Wide, Huge };
 static constexpr size_t kSmemMax = 227 * 1024;
 
 static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t lut_bytes)
@@ -123,18 +130,9 @@ static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t
     case CfgId::Mid: BM = CfgMid::BM; BN = CfgMid::BN; NT = CfgMid::NT; smem = CfgMid::smem_bytes(lut_bytes); break;
     case CfgId::Lean: BM = CfgLean::BM; BN = CfgLean::BN; NT = CfgLean::NT; smem = CfgLean::smem_bytes(lut_bytes); break;
     case CfgId::Wide: BM = CfgWide::BM; BN = CfgWide::BN; NT = CfgWide::NT; smem = CfgWide::smem_bytes(lut_bytes); break;
+    case CfgId::Huge: BM = CfgHuge::BM; BN = CfgHuge::BN; NT = CfgHuge::NT; smem = CfgHuge::smem_bytes(lut_bytes); break;
     default: BM = CfgBig::BM; BN = CfgBig::BN; NT = CfgBig::NT; smem = CfgBig::smem_bytes(lut_bytes); break;
     }
-}
-
-static CfgId cfg_for(int Mmax, int N, uint32_t lut_bytes)
-{
-    CfgId c = N <= 32 ? CfgId::Small
-                      : (N <= 64 ? (Mmax <= 64 ? CfgId::Lean : CfgId::Mid) : (Mmax <= 64 ? CfgId::Wide : CfgId::Big));
-    int BM, BN, NT;
-    size_t smem;
-    cfg_shape(c, BM, BN, NT, smem, lut_bytes);
-    return smem <= kSmemMax ? c : CfgId::Lean;
 }
 
 // Tile plan with a small cost model.  CTAs take tiles round-robin
@@ -142,7 +140,7 @@ static CfgId cfg_for(int Mmax, int N, uint32_t lut_bytes)
 // counts plus a per-tile overhead; split-K (same split count for every
 // sub-problem whose K allows it) trades that makespan against writing and
 // re-reading the partial sums.  Deterministic for a given problem and device.
-static void tile_plan(KParams &p, const Problem &pr, int BM, int BN)
+static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int policy)
 {
     const int G = num_sms();
     p.N = pr.N;
@@ -151,7 +149,7 @@ static void tile_plan(KParams &p, const Problem &pr, int BM, int BN)
     int Kmax = 0;
     for (int s = 0; s < pr.nsub; s++) Kmax = std::max(Kmax, pr.K[s]);
     const int min_chunk = 16 * BK;  // >= 16 k-tiles per split
-    const int max_sp = (path_policy() & 2) ? 1 : std::max(1, std::min(pr.max_splits, Kmax / min_chunk));
+    const int max_sp = (policy & 2) ? 1 : std::max(1, std::min(pr.max_splits, Kmax / min_chunk));
     // cost units: one k-tile of one BM x BN tile
     const double tile_overhead = 2.0;
     const double ktile_s = double(BM) * BN * BK / (20.0 * 1.9e9);     // ~20 approx-MAC/clk/SM
@@ -210,13 +208,49 @@ static void tile_plan(KParams &p, const Problem &pr, int BM, int BN)
     p.ntiles = begin;
     p.ws = nullptr;
     p.ws_elems = ws;
+    return best;
 }
 
-// Table, tile configuration and split plan for a problem.
-static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr, int &eb)
+// Shared-memory wavefronts per warp-wide lookup, including the operand loads
+// of the inner loop: the table row (2^m entries) read by
+// 32 lanes at random columns costs ~row_bytes / 128 wavefronts (>= 1); the A
+// side adds 1/TN (broadcast LDS.128, 2 wavefronts per 4 values, two arrays),
+// the B side 2/TM.  Relative only -- it ranks the tile configurations.
+static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
 {
+    int TM = 16, TN = 4;
+    switch (c) {
+    case CfgId::Small: TM = 8; TN = 1; break;
+    case CfgId::Mid: TM = 16; TN = 2; break;
+    case CfgId::Lean: TM = 8; TN = 2; break;
+    case CfgId::Wide: TM = 8; TN = 4; break;
+    case CfgId::Huge: TM = 16; TN = 8; break;
+    default: break;
+    }
+    double row = double(size_t(1) << mbits) * (eb / 8);
+    double lk = table_in_smem ? std::max(1.0, row / 128.0 * 1.025) : 1.0;
+    return lk + 1.0 / TN + 2.0 / TM;
+}
+
+// Plan cache: the same problem (shape, table width, mode, policy) is planned
+// once per process.
+struct PlanRec {
+    int cfg, tiles_n, nsub, ntiles;
+    int64_t ws_elems;
+    SubP sub[MAX_SUB];
+};
+static std::mutex g_plan_mu;
+static std::map<std::vector<int64_t>, PlanRec> g_plans;
+
+// Table, tile configuration and split plan for a problem.
+// mode / policy < 0: the process-wide multiply mode / path policy.
+static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr, int &eb, int mode = -1,
+                            int policy = -1)
+{
+    if (mode < 0) mode = multiply_mode();
+    if (policy < 0) policy = path_policy();
     const void *tab = nullptr;
-    amsim_status s = device_table(lut, &tab, &eb);
+    amsim_status s = device_table(lut, &tab, &eb, policy);
     if (s != AMSIM_OK) return s;
     int mbits = 0;
     amsim_lut_info(lut, &mbits, nullptr);
@@ -225,9 +259,9 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     // are read from global memory, where they stay L2-resident (<= 16 MB).
     p.lut_global = CfgLean::smem_bytes(bytes) > kSmemMax ? 1 : 0;
     p.mul = MUL_LUT;
-    if (multiply_mode() == AMSIM_MUL_NATIVE) {
+    if (mode == AMSIM_MUL_NATIVE) {
         p.mul = MUL_NATIVE;
-    } else if (multiply_mode() == AMSIM_MUL_DIRECT) {
+    } else if (mode == AMSIM_MUL_DIRECT) {
         if (lut->model_id < 0)
             return set_error(AMSIM_ERR_UNSUPPORTED, "AMSIM_MUL_DIRECT needs a table built from a built-in model");
         p.mul = MUL_DIRECT_EXACT + lut->model_id;
@@ -236,16 +270,61 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     p.lut = tab;
     p.m_bits = mbits;
     p.lut_bytes = bytes;
-    p.policy = path_policy() & 1;
-    int Mmax = 0;
-    for (int i = 0; i < pr.nsub; i++) Mmax = std::max(Mmax, pr.M[i]);
-    const uint32_t smem_lut = (p.lut_global || p.mul != MUL_LUT) ? 0u : bytes;
-    p.cfg = (p.lut_global || p.mul != MUL_LUT) ? int(pr.N <= 64 ? CfgId::Lean : CfgId::Big)
-                                               : int(cfg_for(Mmax, pr.N, bytes));
-    int BM, BN, NT;
-    size_t smem;
-    cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, smem_lut);
-    tile_plan(p, pr, BM, BN);
+    p.policy = policy & 1;
+    const bool smem_table = !p.lut_global && p.mul == MUL_LUT;
+    const uint32_t smem_lut = smem_table ? bytes : 0u;
+    std::vector<int64_t> key = {pr.N, pr.nsub, pr.max_splits, eb, p.lut_global, p.mul, policy & 3, mbits,
+                                num_sms()};
+    for (int i = 0; i < pr.nsub; i++) {
+        key.push_back(pr.M[i]);
+        key.push_back(pr.K[i]);
+    }
+    {
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it != g_plans.end()) {
+            const PlanRec &r = it->second;
+            p.cfg = r.cfg; p.N = pr.N; p.tiles_n = r.tiles_n; p.nsub = r.nsub; p.ntiles = r.ntiles;
+            p.ws_elems = r.ws_elems; p.ws = nullptr;
+            std::memcpy(p.sub, r.sub, sizeof(r.sub));
+            return AMSIM_OK;
+        }
+    }
+    // Candidate tile configurations (the non-table modes and global tables use Big / Lean
+    // only); cost = planned makespan in k-tiles x lookups per k-tile x wavefronts per lookup.
+    std::vector<CfgId> cands;
+    if (smem_table) {
+        cands = {CfgId::Small, CfgId::Mid, CfgId::Big, CfgId::Lean, CfgId::Wide};
+        if (eb >= 16) cands.push_back(CfgId::Huge);
+    } else {
+        cands = {CfgId::Big, CfgId::Lean};
+    }
+    double best = 1e300;
+    KParams bestp = p;
+    for (CfgId c : cands) {
+        int BM, BN, NT;
+        size_t smem;
+        cfg_shape(c, BM, BN, NT, smem, smem_lut);
+        if (smem > kSmemMax) continue;
+        KParams q = p;
+        q.cfg = int(c);
+        double cost = tile_plan(q, pr, BM, BN, policy) * double(BM) * BN * wf_per_lookup(c, eb, mbits, smem_table);
+        if (cost < best * 0.999) {
+            best = cost;
+            bestp = q;
+        }
+    }
+    if (best >= 1e299) return set_error(AMSIM_ERR_UNSUPPORTED, "no tile configuration fits shared memory");
+    p = bestp;
+    if (std::getenv("AMSIM_DEBUG_PLAN"))
+        std::fprintf(stderr, "[amsim plan] N=%d M0=%d K0=%d nsub=%d eb=%d mul=%d -> cfg=%d tiles=%d splits0=%d ws=%lld\n",
+                     pr.N, pr.M[0], pr.K[0], pr.nsub, eb, p.mul, p.cfg, p.ntiles, p.sub[0].splits,
+                     (long long)p.ws_elems);
+    PlanRec r;
+    r.cfg = p.cfg; r.tiles_n = p.tiles_n; r.nsub = p.nsub; r.ntiles = p.ntiles; r.ws_elems = p.ws_elems;
+    std::memcpy(r.sub, p.sub, sizeof(r.sub));
+    std::lock_guard<std::mutex> g(g_plan_mu);
+    g_plans.emplace(std::move(key), r);
     return AMSIM_OK;
 }
 
@@ -290,6 +369,9 @@ static amsim_status launch_eb(const KParams &p, const OpA &a, const OpB &b, cuda
     case CfgId::Mid: return launch_cfg<CfgMid, EB>(p, a, b, st);
     case CfgId::Lean: return launch_cfg<CfgLean, EB>(p, a, b, st);
     case CfgId::Wide: return launch_cfg<CfgWide, EB>(p, a, b, st);
+    case CfgId::Huge:
+        if constexpr (EB >= 16) return launch_cfg<CfgHuge, EB>(p, a, b, st);
+        else return set_error(AMSIM_ERR_UNSUPPORTED, "internal: Huge tiles need 16/32-bit tables");
     default: return launch_cfg<CfgBig, EB>(p, a, b, st);
     }
 }

@@ -87,7 +87,7 @@ static amsim_status upload(amsim_lut *lut, int dev, int eb, DeviceTable &t)
     return AMSIM_OK;
 }
 
-amsim_status device_table(const amsim_lut *lut_c, const void **ptr, int *entry_bits)
+amsim_status device_table(const amsim_lut *lut_c, const void **ptr, int *entry_bits, int policy)
 {
     amsim_lut *lut = const_cast<amsim_lut *>(lut_c);
     int dev = 0;
@@ -95,7 +95,7 @@ amsim_status device_table(const amsim_lut *lut_c, const void **ptr, int *entry_b
     if (e != cudaSuccess) return set_error(AMSIM_ERR_UNSUPPORTED, std::string("no CUDA device: ") + cudaGetErrorString(e));
     if (dev < 0 || dev >= kMaxDevices) return set_error(AMSIM_ERR_UNSUPPORTED, "device index out of range");
     // policy bit 2: the 32-bit layout whatever the table's width (tests prove the width never changes bits)
-    const bool wide = (path_policy() & 4) != 0 && lut->device_entry_bits != 32;
+    const bool wide = ((policy < 0 ? path_policy() : policy) & 4) != 0 && lut->device_entry_bits != 32;
     const int eb = wide ? 32 : lut->device_entry_bits;
     std::lock_guard<std::mutex> g(lut->mu);
     DeviceTable &t = wide ? lut->dev_wide[dev] : lut->dev[dev];

@@ -40,7 +40,8 @@ amsim_status set_error(amsim_status s, const std::string &msg);
 void clear_error();
 
 // Device table for the current device (uploads on first use).
-amsim_status device_table(const amsim_lut *lut, const void **ptr, int *entry_bits);
+// policy < 0: the process-wide path policy (bit 2 selects the 32-bit layout).
+amsim_status device_table(const amsim_lut *lut, const void **ptr, int *entry_bits, int policy = -1);
 
 // Global launch counter (incremented by every kernel launch).
 void count_launch(uint64_t n = 1);

@@ -45,6 +45,18 @@ def main():
     else:
         nets = {"resnet50": inp.resnet50_layers, "resnet18": inp.resnet18_cifar_layers, "lenet5": inp.lenet5_layers}
         L = {l.name: l for l in nets[args.net](args.batch)}[args.layer]
+        if not hasattr(L, "H"):   # dense layer: fwd X W, wgrad X^T dY, dgrad dY W^T
+            x = gen.relu_normal((L.N, L.IN), 1)
+            w = gen.he_normal((L.IN, L.OUT), L.IN, 2)
+            dy = gen.normal((L.N, L.OUT), 3, 2 ** -10)
+            out = {"fwd": torch.empty((L.N, L.OUT), device="cuda"), "wgrad": torch.empty((L.IN, L.OUT), device="cuda"),
+                   "dgrad": torch.empty((L.N, L.IN), device="cuda")}[args.which]
+            fn = {"fwd": lambda: am.amsim_gemm(lut, x, w, out),
+                  "wgrad": lambda: am.amsim_gemm(lut, x, dy, out, trans_a=True),
+                  "dgrad": lambda: am.amsim_gemm(lut, dy, w, out, trans_b=True)}[args.which]
+            macs = L.macs()
+            label = f"{args.net} {args.layer} {args.which} b{args.batch}"
+            return _time(fn, args, ev, macs, label)
         d = am.conv_desc(L.N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad)
         x = gen.relu_normal((L.N, L.H, L.W, L.C), 1)
         w = gen.he_normal((L.R, L.S, L.C, L.K), L.R * L.S * L.C, 2)
@@ -61,6 +73,11 @@ def main():
             ws = torch.empty(max(am.amsim_conv2d_bwd_filter_workspace(lut, d) // 4, 1), device="cuda")
             fn = lambda: am.amsim_conv2d_bwd_filter(lut, d, x, dy, dw, ws)  # noqa: E731
         label = f"{args.net} {args.layer} {args.which} b{args.batch}"
+    _time(fn, args, ev, macs, label)
+
+
+def _time(fn, args, ev, macs, label):
+    import torch
     fn()
     torch.cuda.synchronize()
     for i in range(args.reps):
