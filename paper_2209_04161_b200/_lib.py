@@ -54,6 +54,13 @@ EXPORTS = [
     "amsim_launch_count", "amsim_bench_lut_lookup", "amsim_abi_version", "amsim_set_multiply_mode",
 ]
 
+# every symbol include/amsim_nn.h declares (the non-approximated layers)
+NN_EXPORTS = [
+    "amsim_nn_workspace_bytes", "amsim_bn_fwd_train", "amsim_bn_fwd_infer", "amsim_bn_bwd", "amsim_bias_act_fwd",
+    "amsim_bias_act_bwd", "amsim_maxpool_fwd", "amsim_maxpool_bwd", "amsim_avgpool_fwd", "amsim_avgpool_bwd",
+    "amsim_softmax_xent", "amsim_add", "amsim_sgd_momentum",
+]
+
 # amsim_set_multiply_mode values (include/amsim.h)
 AMSIM_MUL_LUT, AMSIM_MUL_NATIVE, AMSIM_MUL_DIRECT = 0, 1, 2
 
@@ -91,6 +98,21 @@ def lib():
     L.amsim_launch_count.restype = ctypes.c_uint64
     L.amsim_bench_lut_lookup.argtypes = [i32, i32, i32, u32p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double), vp]
     L.amsim_abi_version.restype = i32
+    f32, sz = ctypes.c_float, ctypes.c_size_t
+    L.amsim_nn_workspace_bytes.argtypes = [i64, i32]
+    L.amsim_nn_workspace_bytes.restype = sz
+    L.amsim_bn_fwd_train.argtypes = [vp, i64, i32, vp, vp, f32, vp, i32, vp, vp, vp, vp, vp, f32, vp, sz, vp]
+    L.amsim_bn_fwd_infer.argtypes = [vp, i64, i32, vp, vp, vp, vp, f32, vp, i32, vp, vp]
+    L.amsim_bn_bwd.argtypes = [vp, vp, vp, i64, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp, sz, vp]
+    L.amsim_bias_act_fwd.argtypes = [vp, i64, i32, vp, i32, vp, vp]
+    L.amsim_bias_act_bwd.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, sz, vp]
+    L.amsim_maxpool_fwd.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, vp]
+    L.amsim_maxpool_bwd.argtypes = [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp]
+    L.amsim_avgpool_fwd.argtypes = [vp, i32, i32, i32, vp, vp]
+    L.amsim_avgpool_bwd.argtypes = [vp, i32, i32, i32, vp, vp]
+    L.amsim_softmax_xent.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
+    L.amsim_add.argtypes = [vp, vp, vp, i64, vp]
+    L.amsim_sgd_momentum.argtypes = [vp, vp, vp, i64, f32, f32, f32, vp]
     _lib = L
     return L
 
@@ -275,3 +297,81 @@ def amsim_bench_lut_lookup(m: int, entry_bits: int, b_idx, iters: int = 4096, st
     _check(lib().amsim_bench_lut_lookup(m, entry_bits, iters, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
                                         idx.size, ctypes.byref(out), _stream(stream)), "amsim_bench_lut_lookup")
     return out.value
+
+
+# ---------------------------------------------------------------------------
+# non-approximated layers (include/amsim_nn.h): argument marshalling only
+
+def _p(t):
+    """Device pointer of an optional tensor (None -> NULL)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _ws(ws):
+    return (None, 0) if ws is None else (ctypes.c_void_p(ws.data_ptr()), ws.numel() * ws.element_size())
+
+
+def amsim_nn_workspace_bytes(P: int, C: int) -> int:
+    return int(lib().amsim_nn_workspace_bytes(P, C))
+
+
+def amsim_bn_fwd_train(x, P, C, gamma, beta, eps, res, relu, y, save_mean, save_invstd, running_mean, running_var,
+                       momentum, ws, stream=None):
+    w, wb = _ws(ws)
+    _check(lib().amsim_bn_fwd_train(_p(x), P, C, _p(gamma), _p(beta), eps, _p(res), int(relu), _p(y), _p(save_mean),
+                                    _p(save_invstd), _p(running_mean), _p(running_var), momentum, w, wb,
+                                    _stream(stream)), "amsim_bn_fwd_train")
+
+
+def amsim_bn_fwd_infer(x, P, C, gamma, beta, running_mean, running_var, eps, res, relu, y, stream=None):
+    _check(lib().amsim_bn_fwd_infer(_p(x), P, C, _p(gamma), _p(beta), _p(running_mean), _p(running_var), eps, _p(res),
+                                    int(relu), _p(y), _stream(stream)), "amsim_bn_fwd_infer")
+
+
+def amsim_bn_bwd(dy, y, x, P, C, gamma, save_mean, save_invstd, relu, dx, dres, dgamma, dbeta, ws, stream=None):
+    w, wb = _ws(ws)
+    _check(lib().amsim_bn_bwd(_p(dy), _p(y), _p(x), P, C, _p(gamma), _p(save_mean), _p(save_invstd), int(relu),
+                              _p(dx), _p(dres), _p(dgamma), _p(dbeta), w, wb, _stream(stream)), "amsim_bn_bwd")
+
+
+def amsim_bias_act_fwd(x, P, C, bias, relu, y, stream=None):
+    _check(lib().amsim_bias_act_fwd(_p(x), P, C, _p(bias), int(relu), _p(y), _stream(stream)), "amsim_bias_act_fwd")
+
+
+def amsim_bias_act_bwd(dy, y, P, C, relu, dx, dbias, ws, stream=None):
+    w, wb = _ws(ws)
+    _check(lib().amsim_bias_act_bwd(_p(dy), _p(y), P, C, int(relu), _p(dx), _p(dbias), w, wb, _stream(stream)),
+           "amsim_bias_act_bwd")
+
+
+def amsim_maxpool_fwd(x, N, H, W, C, R, S, stride, pad, y, argmax, stream=None):
+    _check(lib().amsim_maxpool_fwd(_p(x), N, H, W, C, R, S, stride, pad, _p(y), _p(argmax), _stream(stream)),
+           "amsim_maxpool_fwd")
+
+
+def amsim_maxpool_bwd(dy, argmax, N, H, W, C, R, S, stride, pad, dx, stream=None):
+    _check(lib().amsim_maxpool_bwd(_p(dy), _p(argmax), N, H, W, C, R, S, stride, pad, _p(dx), _stream(stream)),
+           "amsim_maxpool_bwd")
+
+
+def amsim_avgpool_fwd(x, N, HW, C, y, stream=None):
+    _check(lib().amsim_avgpool_fwd(_p(x), N, HW, C, _p(y), _stream(stream)), "amsim_avgpool_fwd")
+
+
+def amsim_avgpool_bwd(dy, N, HW, C, dx, stream=None):
+    _check(lib().amsim_avgpool_bwd(_p(dy), N, HW, C, _p(dx), _stream(stream)), "amsim_avgpool_bwd")
+
+
+def amsim_softmax_xent(logits, labels, N, K, loss, dlogits, ws, stream=None):
+    w, wb = _ws(ws)
+    _check(lib().amsim_softmax_xent(_p(logits), _p(labels), N, K, _p(loss), _p(dlogits), w, wb, _stream(stream)),
+           "amsim_softmax_xent")
+
+
+def amsim_add(a, b, out, n, stream=None):
+    _check(lib().amsim_add(_p(a), _p(b), _p(out), n, _stream(stream)), "amsim_add")
+
+
+def amsim_sgd_momentum(w, g, v, n, lr, momentum, weight_decay, stream=None):
+    _check(lib().amsim_sgd_momentum(_p(w), _p(g), _p(v), n, lr, momentum, weight_decay, _stream(stream)),
+           "amsim_sgd_momentum")

@@ -24,9 +24,10 @@ SOURCES = [
     ("amsim_conv_dgrad.cu", "nvcc"),
     ("amsim_conv_wgrad.cu", "nvcc"),
     ("amsim_bench.cu", "nvcc"),
+    ("amsim_nn.cu", "nvcc"),
 ]
 HEADERS = [os.path.join(CSRC, "amsim_internal.h"), os.path.join(CSRC, "amsim_device.cuh"),
-           os.path.join(CSRC, "amsim_dispatch.cuh"), os.path.join(ROOT, "include", "amsim.h")]
+           os.path.join(CSRC, "amsim_dispatch.cuh"), os.path.join(ROOT, "include", "amsim.h"), os.path.join(ROOT, "include", "amsim_nn.h")]
 
 
 def _newer(target: str, deps) -> bool:

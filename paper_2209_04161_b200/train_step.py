@@ -128,3 +128,22 @@ class TrainStep:
     def step(self):
         self.forward()
         self.backward()
+
+    def capture(self):
+        """Capture one step into a CUDA graph (single process: the NCCL
+        all-reduce path stays eager) and return its replay function.  Call
+        after at least one eager step (table upload and plans happen there)."""
+        import torch
+        if self.reducer.world != 1:
+            raise RuntimeError("graph capture is single-GPU only")
+        self.timers = None
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.step()                       # warm the side stream
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            self.step()
+        self._graph = g
+        return g.replay

@@ -28,6 +28,9 @@ def test_exports_every_declared_symbol(built):
     declared = set(re.findall(r"\b(amsim_[a-z0-9_]+)\s*\(", hdr))
     assert declared, "no declarations parsed"
     assert declared == set(_lib.EXPORTS)
+    nn = set(re.findall(r"\b(amsim_[a-z0-9_]+)\s*\(", open(os.path.join(ROOT, "include", "amsim_nn.h")).read()))
+    assert nn == set(_lib.NN_EXPORTS)
+    declared |= nn
     for name in declared:
         assert hasattr(built, name), name
     assert built.amsim_abi_version() == 1
