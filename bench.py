@@ -196,6 +196,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full-step", action="store_true",
+                    help="skip the whole-network training / inference step measurement (net.py)")
     ap.add_argument("--graph", action="store_true",
                     help="N=1: replay the step as one CUDA graph in the timed regions (per-kind kernel times then "
                          "come from one extra eager step)")
@@ -321,6 +323,45 @@ def main():
                "h2d_bytes_per_step": host_in.numel() * 4, "d2h_bytes_per_step": host_out.numel() * 4,
                "ms_per_step": ems}
 
+    # ---- whole training step (NEXT(1)): the same approximate passes plus BN, ReLU,
+    # pooling, residual adds, loss and SGD (net.py); graph replay on one GPU,
+    # eager with the bucketed all-reduce on several ----
+    full = None
+    if not args.no_full_step:
+        from paper_2209_04161_b200 import net as netmod
+        del step, run
+        torch.cuda.empty_cache()
+        net = netmod.BUILDERS[args.workload](lut, batch=nb, device=dev, seed=1000)
+        net.train_step()
+        tr = net.capture(net.train_step) if world == 1 else net.train_step
+        for _ in range(args.warmup):
+            tr()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(args.steps):
+            tr()
+        g1.record()
+        barrier()
+        full_ms = max_over_ranks(g0.elapsed_time(g1) / args.steps, dev)
+        net.infer_step()
+        inf = net.capture(net.infer_step) if world == 1 else net.infer_step
+        inf()
+        barrier()
+        g0.record()
+        for _ in range(args.steps):
+            inf()
+        g1.record()
+        barrier()
+        infer_ms = max_over_ranks(g0.elapsed_time(g1) / args.steps, dev)
+        full = {"train_ms": full_ms, "infer_ms": infer_ms, "approx_passes_share": ms / full_ms,
+                "loss": float(net.loss_value.item()), "cuda_graph": world == 1,
+                "what": "forward + softmax-xent + backward + SGD-momentum of the whole network (BN, ReLU, pooling, "
+                        "residual adds in native FP32 kernels, include/amsim_nn.h); infer = forward with running "
+                        "BN statistics"}
+        del net, tr, inf
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -376,6 +417,7 @@ def main():
                          "per_kind_ms_per_step": {k: v[0] / args.steps for k, v in kinds.items()},
                          "per_kind_gmacs": {k: v[1] / (v[0] * 1e-3) / 1e9 for k, v in kinds.items()}},
             "cpu_baseline": cpu,
+            "full_train_step": full,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
