@@ -33,6 +33,10 @@
 namespace amsim {
 namespace dev {
 
+#ifndef AMSIM_PACK
+#define AMSIM_PACK 1
+#endif
+
 constexpr int BK = 16;
 constexpr int STAGES = 3;
 constexpr int RAW_PAD = 4;    // row padding of k-contiguous raw tiles (keeps 16-B alignment)
@@ -357,7 +361,9 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
 
 // Decode one raw operand tile into (alpha, offset) arrays laid out [BK][rows];
 // tracks min / max exponent fields over nonzero elements.
-template <int NT, int ROWS, bool RAW_ALPHA = false>
+// PACK: one word per element, alpha (bits 31..23) | offset (bits 22..0; shared
+// memory table offsets are < 2^18), halving the inner loop's operand loads.
+template <int NT, int ROWS, bool RAW_ALPHA = false, bool PACK = false>
 __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, uint32_t *al, uint32_t *off, int shift,
                                                uint32_t mask, int off_shift, uint32_t off_base, uint32_t &emin,
                                                uint32_t &emax)
@@ -371,8 +377,13 @@ __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, ui
             float v = kcontig ? raw[i * (BK + RAW_PAD) + kk] : raw[kk * ROWS + i];
             uint32_t u = __float_as_uint(v);
             uint32_t ex = (u >> 23) & 0xFFu;
-            al[e] = RAW_ALPHA ? u : (u & 0xFF800000u);
-            off[e] = off_base + (((u >> shift) & mask) << off_shift);
+            const uint32_t o = off_base + (((u >> shift) & mask) << off_shift);
+            if constexpr (PACK) {
+                al[e] = (u & 0xFF800000u) | o;
+            } else {
+                al[e] = RAW_ALPHA ? u : (u & 0xFF800000u);
+                off[e] = o;
+            }
             if (ex) {
                 emin = min(emin, ex);
                 emax = max(emax, ex);
@@ -422,6 +433,12 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 {
     constexpr int NT = Cf::NT, NWARPS = Cf::NWARPS, TM = Cf::TM, TN = Cf::TN, BM = Cf::BM, BN = Cf::BN;
     constexpr int CG = Cf::CG;
+    // packed (alpha | offset) operand words for the LSU-bound 16/32-bit tables in
+    // shared memory (global table offsets can exceed 23 bits; the 8-bit path is
+    // issue-bound and loses more to the unpacking than it gains: measured
+    // +5.7 % / -3.8 % on the ResNet-50 step)
+    constexpr bool PK = AMSIM_PACK && MUL == MUL_LUT && !GL && EB >= 16;
+    constexpr uint32_t AMASK = 0xFF800000u, OMASK = 0x007FFFFFu;
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -533,10 +550,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             uint32_t *d = dec + (g & 1) * Cf::DEC;
             uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + 2 * BK * BM, *b_off = b_al + BK * BN;
             uint32_t amin = 255, amax = 0, bmin = 255, bmax = 0;
-            decode_operand<NT, BM, MUL == MUL_NATIVE>(ra, p.da.kcontig, a_al, a_off, shift, mask, a_off_shift,
-                                                      a_off_base, amin, amax);
-            decode_operand<NT, BN, MUL == MUL_NATIVE>(rb, p.db.kcontig, b_al, b_off, shift, mask, b_off_shift,
-                                                      b_off_base, bmin, bmax);
+            decode_operand<NT, BM, MUL == MUL_NATIVE, PK>(ra, p.da.kcontig, a_al, a_off, shift, mask, a_off_shift,
+                                                          a_off_base, amin, amax);
+            decode_operand<NT, BN, MUL == MUL_NATIVE, PK>(rb, p.db.kcontig, b_al, b_off, shift, mask, b_off_shift,
+                                                          b_off_base, bmin, bmax);
             amin = __reduce_min_sync(0xffffffffu, amin);
             amax = __reduce_max_sync(0xffffffffu, amax);
             bmin = __reduce_min_sync(0xffffffffu, bmin);
@@ -597,18 +614,32 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 #pragma unroll
                     for (int r = 0; r < TM; r += 4) {
                         uint4 v = *reinterpret_cast<const uint4 *>(A_al + kk * BM + r);
-                        uint4 o = *reinterpret_cast<const uint4 *>(A_off + kk * BM + r);
-                        aal[r] = v.x; aal[r + 1] = v.y; aal[r + 2] = v.z; aal[r + 3] = v.w;
-                        aof[r] = o.x; aof[r + 1] = o.y; aof[r + 2] = o.z; aof[r + 3] = o.w;
+                        if constexpr (PK) {
+                            aal[r] = v.x & AMASK; aal[r + 1] = v.y & AMASK; aal[r + 2] = v.z & AMASK; aal[r + 3] = v.w & AMASK;
+                            aof[r] = v.x & OMASK; aof[r + 1] = v.y & OMASK; aof[r + 2] = v.z & OMASK; aof[r + 3] = v.w & OMASK;
+                        } else {
+                            uint4 o = *reinterpret_cast<const uint4 *>(A_off + kk * BM + r);
+                            aal[r] = v.x; aal[r + 1] = v.y; aal[r + 2] = v.z; aal[r + 3] = v.w;
+                            aof[r] = o.x; aof[r + 1] = o.y; aof[r + 2] = o.z; aof[r + 3] = o.w;
+                        }
                     }
                     if constexpr (TN % 4 == 0) {
 #pragma unroll
                         for (int c = 0; c < TN; c += 4) {
                             uint4 v = *reinterpret_cast<const uint4 *>(B_al + kk * BN + c * 32);
-                            uint4 o = *reinterpret_cast<const uint4 *>(B_off + kk * BN + c * 32);
-                            bal[c] = v.x; bal[c + 1] = v.y; bal[c + 2] = v.z; bal[c + 3] = v.w;
-                            bof[c] = o.x; bof[c + 1] = o.y; bof[c + 2] = o.z; bof[c + 3] = o.w;
+                            if constexpr (PK) {
+                                bal[c] = v.x & AMASK; bal[c + 1] = v.y & AMASK; bal[c + 2] = v.z & AMASK; bal[c + 3] = v.w & AMASK;
+                                bof[c] = v.x & OMASK; bof[c + 1] = v.y & OMASK; bof[c + 2] = v.z & OMASK; bof[c + 3] = v.w & OMASK;
+                            } else {
+                                uint4 o = *reinterpret_cast<const uint4 *>(B_off + kk * BN + c * 32);
+                                bal[c] = v.x; bal[c + 1] = v.y; bal[c + 2] = v.z; bal[c + 3] = v.w;
+                                bof[c] = o.x; bof[c + 1] = o.y; bof[c + 2] = o.z; bof[c + 3] = o.w;
+                            }
                         }
+                    } else if constexpr (TN == 2 && PK) {
+                        uint2 v = *reinterpret_cast<const uint2 *>(B_al + kk * BN);
+                        bal[0] = v.x & AMASK; bal[1] = v.y & AMASK;
+                        bof[0] = v.x & OMASK; bof[1] = v.y & OMASK;
                     } else if constexpr (TN == 2) {
                         uint2 v = *reinterpret_cast<const uint2 *>(B_al + kk * BN);
                         uint2 o = *reinterpret_cast<const uint2 *>(B_off + kk * BN);
@@ -617,8 +648,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     } else {
 #pragma unroll
                         for (int c = 0; c < TN; c++) {
-                            bal[c] = B_al[kk * BN + c];
-                            bof[c] = B_off[kk * BN + c];
+                            bal[c] = PK ? (B_al[kk * BN + c] & AMASK) : B_al[kk * BN + c];
+                            bof[c] = PK ? (B_al[kk * BN + c] & OMASK) : B_off[kk * BN + c];
                         }
                     }
 #pragma unroll
@@ -638,11 +669,14 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                 for (int kk = 0; kk < BK; kk++) {
 #pragma unroll
                     for (int r = 0; r < TM; r++) {
-                        uint32_t aal = A_al[kk * BM + r], aof = A_off[kk * BM + r];
+                        uint32_t aal = A_al[kk * BM + r], aof = PK ? (aal & OMASK) : A_off[kk * BM + r];
+                        if (PK) aal &= AMASK;
                         uint32_t ea = (aal >> 23) & 0xFFu;
 #pragma unroll
                         for (int c = 0; c < TN; c++) {
-                            uint32_t bal = B_al[kk * BN + Cf::col(c)], bof = B_off[kk * BN + Cf::col(c)];
+                            uint32_t bal = B_al[kk * BN + Cf::col(c)];
+                            uint32_t bof = PK ? (bal & OMASK) : B_off[kk * BN + Cf::col(c)];
+                            if (PK) bal &= AMASK;
                             uint32_t eb = (bal >> 23) & 0xFFu;
                             uint32_t ent = (MUL == MUL_LUT ? lut_entry<EB, GL>(aof + bof, lut_g)
                                                            : direct_entry<MUL>(aof, bof)) * MULV;  // (carry << 23) | mantissa
