@@ -50,6 +50,8 @@ def lib():
         L.oracle_mul.restype = ctypes.c_int
         L.oracle_mul_vec.argtypes = [f32p, f32p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, f32p]
         L.oracle_mul_vec.restype = ctypes.c_int
+        L.oracle_cast_e_vec.argtypes = [f32p, ctypes.c_int64, ctypes.c_int, f32p]
+        L.oracle_cast_e_vec.restype = None
         L.oracle_model_call.argtypes = [ctypes.c_int, ctypes.c_float, ctypes.c_float]
         L.oracle_model_call.restype = ctypes.c_float
         L.oracle_gemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
@@ -90,6 +92,16 @@ def num_threads() -> int:
 
 def model_call(model: str, a: float, b: float) -> float:
     return float(lib().oracle_model_call(MODELS[model], a, b))
+
+
+def cast_e(x, e: int) -> np.ndarray:
+    """Exponent cast of every element to the (1, e, m) range (reading C23,
+    amsim_oracle.c oracle_cast_e); applied to both operands before AMSim."""
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(a)
+    f32p = ctypes.POINTER(ctypes.c_float)
+    lib().oracle_cast_e_vec(a.ctypes.data_as(f32p), a.size, int(e), out.ctypes.data_as(f32p))
+    return out
 
 
 def mul(a, b, model: str = "exact", m: int = 7) -> np.ndarray:

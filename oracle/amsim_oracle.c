@@ -237,6 +237,32 @@ int oracle_mul_vec(const float *a, const float *b, int64_t n, int model_id, int 
     return err;
 }
 
+/* ------------------------------------------------------------------ */
+/* Exponent casting to a (1, e, m) format ("the bits of the
+ * exponent e can be varied from 1 to 8 provided that a proper exponent casting
+ * function is given"; the paper gives none -- reading C23):
+ * bias B = 2^(e-1) - 1, normal unbiased exponents [1 - B, B].  A normal FP32
+ * operand whose unbiased exponent is above B becomes +-Inf (overflow), below
+ * 1 - B +-0 (no subnormals, as Alg. 2 flushes them); zeros,
+ * subnormals, Inf and NaN pass unchanged.  e = 8 is the identity.  The cast is
+ * applied to both operands before Alg. 2; products and sums stay FP32.     */
+float oracle_cast_e(float x, int e)
+{
+    uint32_t u = bits_of(x);
+    int ef = (int)exp_field(u);
+    if (e >= 8 || ef == 0 || ef == 255) return x;
+    int B = (1 << (e - 1)) - 1;
+    int unb = ef - 127;
+    if (unb > B) return float_of((u & 0x80000000u) | 0x7F800000u);
+    if (unb < 1 - B) return float_of(u & 0x80000000u);
+    return x;
+}
+
+void oracle_cast_e_vec(const float *in, int64_t n, int e, float *out)
+{
+    for (int64_t i = 0; i < n; i++) out[i] = oracle_cast_e(in[i], e);
+}
+
 /* Direct model call (for the LUT-vs-model exhaustive pins). */
 float oracle_model_call(int model_id, float a, float b)
 {

@@ -329,3 +329,65 @@ def test_conv_row_sampling(orc):
         rows = np.array([nrows - 1, 0, nrows // 2])
         part = fn(d, a1, a2, "mitchell", rows=rows)
         assert np.array_equal(u32(part.c32), u32(full.c32[rows]))
+
+
+# ---------------------------------------------------------------------------
+# exponent casting to (1, e, m) (reading C23)
+
+def test_cast_e8_is_identity(orc):
+    g = inp.rng(41)
+    x = f32(g.integers(0, 2 ** 32, 20000, dtype=np.uint64).astype(np.uint32))
+    assert np.array_equal(u32(orc.cast_e(x, 8)), u32(x))
+
+
+def test_cast_e5_matches_ieee_half_range(orc):
+    """e = 5 is IEEE binary16's exponent: normal magnitudes in
+    [finfo(float16).tiny, 2^finfo(float16).maxexp) survive, larger overflow to
+    +-Inf, smaller flush to +-0 (no subnormals)."""
+    fi = np.finfo(np.float16)
+    g = inp.rng(42)
+    ex = g.integers(1, 255, 20000).astype(np.uint32)
+    x = f32((g.integers(0, 2, 20000).astype(np.uint32) << 31) | (ex << 23) | g.integers(0, 1 << 23, 20000).astype(np.uint32))
+    y = orc.cast_e(x, 5)
+    a = np.abs(x.astype(np.float64))
+    big = a >= 2.0 ** fi.maxexp
+    small = a < float(fi.tiny)
+    keep = ~big & ~small
+    assert np.all(np.isinf(y[big])) and np.array_equal(np.signbit(y[big]), np.signbit(x[big]))
+    assert np.all(y[small] == 0) and np.array_equal(np.signbit(y[small]), np.signbit(x[small]))
+    assert np.array_equal(u32(y[keep]), u32(x[keep]))
+    # values exactly representable as float16 normals are unchanged
+    h = g.normal(0, 100, 5000).astype(np.float16)
+    h = h[np.abs(h.astype(np.float64)) >= float(fi.tiny)].astype(np.float32)
+    assert np.array_equal(u32(orc.cast_e(h, 5)), u32(h))
+
+
+def test_cast_then_amsim_is_half_precision_product(orc):
+    """(1,5,10) with the exact multiplier: for float16 normals the product is
+    the exact FP32 product of the two halves (an 11x11-bit significand product
+    is exact in FP32) -- the IEEE half-precision multiplier without rounding."""
+    g = inp.rng(43)
+    a = g.normal(0, 4, 3000).astype(np.float16).astype(np.float32)
+    b = g.normal(0, 4, 3000).astype(np.float16).astype(np.float32)
+    fi = np.finfo(np.float16)
+    ok = (np.abs(a) >= float(fi.tiny)) & (np.abs(b) >= float(fi.tiny))
+    a, b = a[ok], b[ok]
+    got = orc.mul(orc.cast_e(a, 5), orc.cast_e(b, 5), "exact", 10)
+    want = (a.astype(np.float64) * b.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(u32(got), u32(want))
+
+
+@pytest.mark.parametrize("e", [1, 2, 3, 4, 6, 7])
+def test_cast_boundaries_closed_form(orc, e):
+    """The largest kept magnitude is just below 2^(B+1), the smallest kept is
+    2^(1-B), B = 2^(e-1) - 1; e = 1 has no normal numbers at all."""
+    B = 2 ** (e - 1) - 1
+    top = np.float32(np.nextafter(np.float32(2.0 ** (B + 1)), np.float32(0)))
+    cases = np.array([top, 2.0 ** (B + 1), 2.0 ** (1 - B), np.nextafter(np.float32(2.0 ** (1 - B)), np.float32(0)),
+                      -(2.0 ** (B + 1))], np.float32)
+    y = orc.cast_e(cases, e)
+    if e == 1:   # B = 0, kept range [2^1, 2^1) is empty: 1.99 (exponent 0 < 1 - B) flushes, 2 overflows
+        assert y[0] == 0 and np.isposinf(y[2])
+    else:
+        assert y[0] == cases[0] and y[2] == cases[2]
+    assert np.isposinf(y[1]) and np.isneginf(y[4]) and y[3] == 0
