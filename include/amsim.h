@@ -113,6 +113,20 @@ amsim_status amsim_lut_load(const char *path, amsim_lut **out);
 
 void amsim_lut_destroy(amsim_lut *lut);
 
+/* Exponent casting to a (1, e, m) format ("the bits of the
+ * exponent e can be varied from 1 to 8 provided that a proper exponent casting
+ * function is given"; reading C23).  Creates a new handle with a
+ * copy of src's table whose compute calls first cast BOTH operands of every
+ * product to e exponent bits: with bias B = 2^(e-1) - 1, a normal operand of
+ * unbiased exponent above B becomes +-Inf, below 1 - B +-0; zeros,
+ * subnormals, Inf and NaN are unchanged.  Products and sums stay FP32.
+ * e = 8 (the default of every other constructor) is the identity.
+ * Errors: AMSIM_ERR_INVALID_ARG (null, e outside [1, 8]), AMSIM_ERR_NOMEM. */
+amsim_status amsim_lut_with_exponent_bits(const amsim_lut *src, int e_bits, amsim_lut **out);
+
+/* The exponent width of a handle (8 unless set by amsim_lut_with_exponent_bits). */
+amsim_status amsim_lut_exponent_bits(const amsim_lut *lut, int *e_bits);
+
 /* Thread-local description of the last error on this thread ("" if none). */
 const char *amsim_last_error(void);
 

@@ -52,6 +52,7 @@ EXPORTS = [
     "amsim_model_mbm", "amsim_gemm", "amsim_conv2d_fwd", "amsim_conv2d_bwd_data",
     "amsim_conv2d_bwd_filter_workspace", "amsim_conv2d_bwd_filter", "amsim_set_path_policy",
     "amsim_launch_count", "amsim_bench_lut_lookup", "amsim_abi_version", "amsim_set_multiply_mode",
+    "amsim_lut_with_exponent_bits", "amsim_lut_exponent_bits",
 ]
 
 # every symbol include/amsim_nn.h declares (the non-approximated layers)
@@ -82,6 +83,8 @@ def lib():
     L.amsim_lut_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.amsim_lut_save.argtypes = [vp, ctypes.c_char_p]
     L.amsim_lut_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.amsim_lut_with_exponent_bits.argtypes = [vp, i32, ctypes.POINTER(vp)]
+    L.amsim_lut_exponent_bits.argtypes = [vp, ctypes.POINTER(i32)]
     L.amsim_lut_destroy.argtypes = [vp]
     L.amsim_lut_destroy.restype = None
     L.amsim_last_error.restype = ctypes.c_char_p
@@ -165,6 +168,18 @@ class Lut:
         _check(lib().amsim_lut_from_entries(e.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), m, ctypes.byref(out)),
                "amsim_lut_from_entries")
         return cls(out.value)
+
+    def with_exponent_bits(self, e: int) -> "Lut":
+        """amsim_lut_with_exponent_bits: a (1, e, m) copy (operands cast to e exponent bits)."""
+        out = ctypes.c_void_p()
+        _check(lib().amsim_lut_with_exponent_bits(self.handle, int(e), ctypes.byref(out)),
+               "amsim_lut_with_exponent_bits")
+        return Lut(out.value)
+
+    def exponent_bits(self) -> int:
+        e = ctypes.c_int()
+        _check(lib().amsim_lut_exponent_bits(self.handle, ctypes.byref(e)), "amsim_lut_exponent_bits")
+        return e.value
 
     @classmethod
     def load(cls, path: str) -> "Lut":

@@ -170,6 +170,7 @@ struct KParams {
     uint32_t lut_bytes;
     int policy;           // 1 = force the careful path
     int lut_global;       // table read from global memory / L2 (too large for shared memory)
+    int ecast_lo, ecast_hi;  // exponent casting (reading C23): normal exponent fields outside [lo, hi] -> 0 / Inf
     int mul;              // MulMode
 };
 
@@ -366,7 +367,7 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
 template <int NT, int ROWS, bool RAW_ALPHA = false, bool PACK = false>
 __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, uint32_t *al, uint32_t *off, int shift,
                                                uint32_t mask, int off_shift, uint32_t off_base, uint32_t &emin,
-                                               uint32_t &emax)
+                                               uint32_t &emax, uint32_t elo, uint32_t ehi)
 {
     constexpr int total = BK * ROWS;
 #pragma unroll
@@ -377,6 +378,10 @@ __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, ui
             float v = kcontig ? raw[i * (BK + RAW_PAD) + kk] : raw[kk * ROWS + i];
             uint32_t u = __float_as_uint(v);
             uint32_t ex = (u >> 23) & 0xFFu;
+            if (ex != 0 && ex != 255 && (ex < elo || ex > ehi)) {  // exponent cast to (1, e, m), reading C23
+                u = (u & 0x80000000u) | (ex > ehi ? 0x7F800000u : 0u);
+                ex = (u >> 23) & 0xFFu;
+            }
             const uint32_t o = off_base + (((u >> shift) & mask) << off_shift);
             if constexpr (PACK) {
                 al[e] = (u & 0xFF800000u) | o;
@@ -476,6 +481,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     const int b_off_shift = MUL == MUL_LUT ? ebytes_log2 : shift;
     const uint32_t a_off_base = MUL == MUL_LUT ? lut_base : (MUL == MUL_DIRECT_EXACT ? 0x3F800000u : 0u);
     const uint32_t b_off_base = MUL == MUL_DIRECT_EXACT ? 0x3F800000u : 0u;
+    const uint32_t elo = uint32_t(p.ecast_lo), ehi = uint32_t(p.ecast_hi);
     const float *dummy = reinterpret_cast<const float *>(p.lut);  // valid global address for 0-byte copies
 
     struct Tile {
@@ -551,9 +557,9 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + 2 * BK * BM, *b_off = b_al + BK * BN;
             uint32_t amin = 255, amax = 0, bmin = 255, bmax = 0;
             decode_operand<NT, BM, MUL == MUL_NATIVE, PK>(ra, p.da.kcontig, a_al, a_off, shift, mask, a_off_shift,
-                                                          a_off_base, amin, amax);
+                                                          a_off_base, amin, amax, elo, ehi);
             decode_operand<NT, BN, MUL == MUL_NATIVE, PK>(rb, p.db.kcontig, b_al, b_off, shift, mask, b_off_shift,
-                                                          b_off_base, bmin, bmax);
+                                                          b_off_base, bmin, bmax, elo, ehi);
             amin = __reduce_min_sync(0xffffffffu, amin);
             amax = __reduce_max_sync(0xffffffffu, amax);
             bmin = __reduce_min_sync(0xffffffffu, bmin);

@@ -267,6 +267,11 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         p.mul = MUL_DIRECT_EXACT + lut->model_id;
     }
     if (p.mul != MUL_LUT) p.lut_global = 0;
+    {   // exponent casting (reading C23): kept normal exponent fields [128 - B, 127 + B], B = 2^(e-1) - 1
+        const int B = (1 << (lut->e_bits - 1)) - 1;
+        p.ecast_lo = lut->e_bits >= 8 ? 1 : 128 - B;
+        p.ecast_hi = lut->e_bits >= 8 ? 254 : 127 + B;
+    }
     p.lut = tab;
     p.m_bits = mbits;
     p.lut_bytes = bytes;

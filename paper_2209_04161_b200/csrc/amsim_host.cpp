@@ -335,6 +335,30 @@ amsim_status amsim_lut_load(const char *path, amsim_lut **out)
     return AMSIM_OK;
 }
 
+amsim_status amsim_lut_with_exponent_bits(const amsim_lut *src, int e_bits, amsim_lut **out)
+{
+    clear_error();
+    if (!src || !out) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_lut_with_exponent_bits: null argument");
+    if (e_bits < 1 || e_bits > 8)
+        return set_error(AMSIM_ERR_INVALID_ARG, "amsim_lut_with_exponent_bits: e must be in [1, 8] (PAPER.md:392)");
+    amsim_lut *lut = new (std::nothrow) amsim_lut;
+    if (!lut) return set_error(AMSIM_ERR_NOMEM, "out of host memory");
+    lut->m = src->m;
+    lut->entries = src->entries;
+    lut->device_entry_bits = src->device_entry_bits;
+    lut->model_id = src->model_id;
+    lut->e_bits = e_bits;
+    *out = lut;
+    return AMSIM_OK;
+}
+
+amsim_status amsim_lut_exponent_bits(const amsim_lut *lut, int *e_bits)
+{
+    if (!lut || !e_bits) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_lut_exponent_bits: null argument");
+    *e_bits = lut->e_bits;
+    return AMSIM_OK;
+}
+
 void amsim_lut_destroy(amsim_lut *lut)
 {
     if (!lut) return;

@@ -185,3 +185,14 @@ def test_compute_without_gpu_fails_loudly(built):
     st = L.amsim_gemm(lut.handle, 0, 0, 4, 4, 4, ctypes.cast(buf, ctypes.c_void_p), 4,
                       ctypes.cast(buf, ctypes.c_void_p), 4, ctypes.cast(buf, ctypes.c_void_p), 4, 0, None)
     assert st == 2, L.amsim_last_error()  # AMSIM_ERR_UNSUPPORTED: no device
+
+
+def test_exponent_bits_handle(built):
+    lut = am.Lut.build("exact", 7)
+    assert lut.exponent_bits() == 8
+    l5 = lut.with_exponent_bits(5)
+    assert l5.exponent_bits() == 5 and l5.info() == lut.info()
+    assert np.array_equal(l5.entries(), lut.entries())
+    for bad in (0, 9, -1):
+        with pytest.raises(am.AmsimError):
+            lut.with_exponent_bits(bad)

@@ -50,9 +50,13 @@ def host(t):
 
 
 def assert_bits(got, want, what=""):
+    """Bit equality; two NaNs match whatever their payloads (IEEE 754 leaves
+    the payload of e.g. Inf - Inf to the implementation: GPU 0x7FFFFFFF, x86
+    0xFFC00000)."""
     g = np.ascontiguousarray(got, np.float32).view(np.uint32)
     w = np.ascontiguousarray(want, np.float32).view(np.uint32)
-    bad = np.flatnonzero(g.ravel() != w.ravel())
+    both_nan = np.isnan(g.view(np.float32)) & np.isnan(w.view(np.float32))
+    bad = np.flatnonzero((g.ravel() != w.ravel()) & ~both_nan.ravel())
     assert bad.size == 0, (f"{what}: {bad.size} of {g.size} differ; first at {bad[:5]}: "
                            f"got {g.ravel()[bad[:5]]} want {w.ravel()[bad[:5]]}")
 
@@ -574,3 +578,41 @@ def test_native_mode_is_fp32_gemm(am, luts):
     absum = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64)
     assert np.all(np.abs(got - ref) <= 1e-5 * absum)
     assert np.max(np.abs(got.astype(np.float64) - want)) <= 1e-6 * absum.max()
+
+
+# ---------------------------------------------------------------------------
+# (1, e, m) exponent casting (reading C23)
+
+@pytest.mark.parametrize("model,m,e", [("exact", 10, 5), ("exact", 7, 5), ("mitchell", 7, 4), ("mbm", 7, 2),
+                                       ("exact", 3, 1), ("mitchell", 7, 8)])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_exponent_cast_per_product(am, luts, orc, model, m, e, policy):
+    lut = luts(model, m).with_exponent_bits(e)
+    assert lut.exponent_bits() == e
+    v = _sampled_grid(m) if m > 7 else inp.operand_grid(m, exponents=(1, 60, 100, 110, 113, 120, 126, 127, 128, 134,
+                                                                      141, 142, 150, 200, 254))
+    am.amsim_set_path_policy(policy)
+    try:
+        got = run_gemm(am, lut, v[:, None], v[None, :])
+    finally:
+        am.amsim_set_path_policy(0)
+    c = orc.cast_e(v, e)
+    assert_bits(got, orc.mul(c[:, None], c[None, :], model, m), f"e={e} {model} m={m}")
+
+
+@pytest.mark.parametrize("e", [5, 4])
+def test_exponent_cast_gemm_and_conv(am, luts, orc, e):
+    lut = luts("mitchell").with_exponent_bits(e)
+    A = inp.normal((70, 90), 101) * np.float32(300.0)        # spans the e-bit range and beyond
+    B = inp.normal((90, 50), 102) * np.float32(1e-3)
+    shape = (2, 10, 10, 8, 36, 3, 3, 2, 1)
+    x, w, dy, OH, OW = _conv_tensors(shape, 103)
+    x = x * np.float32(1e3)
+    d = am.conv_desc(*shape)
+    od = orc.conv_desc(*shape)
+    cx, cw, cdy = orc.cast_e(x, e), orc.cast_e(w, e), orc.cast_e(dy, e)
+    with exact_order(am):
+        assert_bits(run_gemm(am, lut, A, B), orc.gemm(orc.cast_e(A, e), orc.cast_e(B, e), "mitchell", 7).c32)
+        assert_bits(_run_conv(am, lut, d, x, w, dy, "fwd"), orc.conv_fwd(od, cx, cw, "mitchell").c32, "fwd")
+        assert_bits(_run_conv(am, lut, d, x, w, dy, "dgrad"), orc.conv_bwd_data(od, cdy, cw, "mitchell").c32, "dgrad")
+        assert_bits(_run_conv(am, lut, d, x, w, dy, "wgrad"), orc.conv_bwd_filter(od, cx, cdy, "mitchell").c32, "wgrad")
