@@ -155,6 +155,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 alone runs the oracle, on all host cores
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     import oracle
     oracle.build()
     for _ in range(args.warmup):
@@ -215,11 +217,19 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # AMSIM_DIST_BACKEND=gloo + ranks sharing GPUs (gpu = local % count) exercise the
+        # multi-rank path on a 1-GPU box; production is NCCL with one rank per GPU
+        backend = os.environ.get("AMSIM_DIST_BACKEND", "nccl")
+        gpu = local % torch.cuda.device_count()
+        torch.cuda.set_device(gpu)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     else:
+        gpu = 0
         torch.cuda.set_device(0)
-    dev = torch.device("cuda", local if world > 1 else 0)
+    dev = torch.device("cuda", gpu)
 
     import paper_2209_04161_b200 as am
     from paper_2209_04161_b200.dp import max_over_ranks, shard_batch
@@ -234,7 +244,10 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[gpu])
+            else:
+                dist.barrier()
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
@@ -252,7 +265,7 @@ def main():
         barrier()
 
     # ---- timed region (device-resident inputs) ----
-    clocks = ClockSampler(local if world > 1 else 0)
+    clocks = ClockSampler(gpu)
     clocks.start()
     step.timers = None if use_graph else []
     launches0 = am.amsim_launch_count()
