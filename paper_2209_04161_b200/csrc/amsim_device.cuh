@@ -327,8 +327,7 @@ template <int NT, int ROWS, class Op>
 __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, float *raw, int s, int mn0, int k0,
                                               int kend, const float *dummy)
 {
-    static_assert((ROWS & (ROWS - 1)) == 0, "tile rows must be a power of two");
-    constexpr int ROWS_LOG2 = __builtin_ctz(ROWS);
+    static_assert(ROWS % 4 == 0, "tile rows must be a multiple of 4");
     const int tid = threadIdx.x;
     const int vl = d.vec_log2;
     if (d.kcontig) {  // raw [ROWS][BK + RAW_PAD]
@@ -345,10 +344,11 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
                 cp_async4(dst, src ? src : dummy, src != nullptr);
         }
     } else {  // raw [BK][ROWS]
-        const int cpr_log2 = ROWS_LOG2 - vl;
-        const int total = BK << cpr_log2;
+        const int total = (BK * ROWS) >> vl;
         for (int c = tid; c < total; c += NT) {
-            int kk = c >> cpr_log2, i = (c & ((1 << cpr_log2) - 1)) << vl;
+            // chunks per row: ROWS or ROWS / 4 (compile-time divisors)
+            int kk = vl ? c / (ROWS / 4) : c / ROWS;
+            int i = (vl ? c % (ROWS / 4) : c % ROWS) << vl;
             int k = k0 + kk;
             const float *src = (k < kend) ? op.at(s, mn0 + i, k) : nullptr;
             uint32_t dst = smem_u32(raw + kk * ROWS + i);
