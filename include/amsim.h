@@ -212,8 +212,11 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
  *            the tile planner may split K to balance the SMs; partials are
  *            reduced in a fixed order, so results stay deterministic);
  *   bit 2 -- use the 32-bit device table layout even when the table fits 8
- *            or 16 bits (tests: the layout changes speed, never bits).
- * Errors: AMSIM_ERR_INVALID_ARG outside [0, 7]. */
+ *            or 16 bits (tests: the layout changes speed, never bits);
+ *   bit 3 -- stage every operand tile with cp.async gathers (default: tiles
+ *            that are plain boxes of a row-major matrix -- the weights of conv
+ *            fwd, the errors of wgrad, GEMM B -- are loaded by TMA).
+ * Errors: AMSIM_ERR_INVALID_ARG outside [0, 15]. */
 amsim_status amsim_set_path_policy(int policy);
 
 /* Multiply mode (process-wide, default AMSIM_MUL_LUT).  The two other modes

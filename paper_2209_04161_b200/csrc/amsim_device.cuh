@@ -26,6 +26,7 @@
 //  * acc starts at +0 and adds products in increasing k (FP32).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (type only; descriptors are encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -63,6 +64,27 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const float *src, bool 
 __device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar)
 {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar));
+}
+
+// TMA: expect `bytes` more transaction bytes on the stage barrier (no arrival),
+// then a 2-D tile load that completes them (the tensor map lives in the
+// __grid_constant__ kernel parameters).
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
@@ -156,6 +178,11 @@ struct OpDesc {
 };
 
 struct KParams {
+    // TMA descriptors of the operands whose smem tile is a plain 2-D box of a
+    // row-major matrix ([BK][rows], rows contiguous: GemmOp with k strided),
+    // tma_on[0] = A, [1] = B; the other operands are gathered with cp.async.
+    CUtensorMap tma[2];
+    int tma_on[2];
     int N, tiles_n, nsub, ntiles;
     SubP sub[MAX_SUB];
     float *C;             // output (ldc-strided rows, A map's out_row)
@@ -523,9 +550,20 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             float *ra = raw + stage * Cf::RAW_STAGE;
             float *rb = ra + Cf::RAW_A;
             int k0 = IT.kb + ik * BK;
-            issue_operand<NT, BM>(opa, p.da, ra, IT.s, IT.m0, k0, IT.ke, dummy);
-            issue_operand<NT, BN>(opb, p.db, rb, IT.s, IT.n0, k0, IT.ke, dummy);
-            cp_async_arrive_noinc(smem_u32(&bars[stage]));
+            const uint32_t bar = smem_u32(&bars[stage]);
+            if (p.tma_on[0] | p.tma_on[1]) {
+                if (tid == 0) {
+                    // the stage's previous contents were read (generic proxy) before the
+                    // last __syncthreads; order those reads before the async-proxy writes
+                    fence_proxy_async_smem();
+                    mbar_expect_tx(bar, (p.tma_on[0] ? BM * BK * 4 : 0) + (p.tma_on[1] ? BN * BK * 4 : 0));
+                    if (p.tma_on[0]) tma_load_2d(smem_u32(ra), &p.tma[0], IT.m0, k0, bar);
+                    if (p.tma_on[1]) tma_load_2d(smem_u32(rb), &p.tma[1], IT.n0, k0, bar);
+                }
+            }
+            if (!p.tma_on[0]) issue_operand<NT, BM>(opa, p.da, ra, IT.s, IT.m0, k0, IT.ke, dummy);
+            if (!p.tma_on[1]) issue_operand<NT, BN>(opb, p.db, rb, IT.s, IT.n0, k0, IT.ke, dummy);
+            cp_async_arrive_noinc(bar);
             ig++;
             if (++ik == kt) {
                 ik = 0;

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -381,6 +382,44 @@ static amsim_status launch_eb(const KParams &p, const OpA &a, const OpB &b, cuda
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA descriptors for operand tiles that are plain boxes of a row-major matrix:
+// a GemmOp read with k strided (smem tile [BK][rows], rows contiguous), i.e.
+// the B operand of conv fwd (w) and wgrad (dy), GEMM B (no transpose) and GEMM
+// A when transposed.  The box is rows x BK elements at (row0, k0); out-of-range
+// elements are zero-filled by the TMA unit, like the cp.async path's zero fill.
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+template <class Op>
+static int setup_tma(CUtensorMap *, const Op &, int) { return 0; }
+
+static int setup_tma(CUtensorMap *map, const GemmOp &op, int rows)
+{
+    if (op.kcontig || (path_policy() & 8)) return 0;   // policy bit 3: cp.async for every operand
+    auto fn = tma_encode_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(op.p) & 15) || (op.ld * 4) % 16 || op.MN <= 0 || op.K <= 0) return 0;
+    cuuint64_t dims[2] = {cuuint64_t(op.MN), cuuint64_t(op.K)};
+    cuuint64_t strides[1] = {cuuint64_t(op.ld) * 4};
+    cuuint32_t box[2] = {cuuint32_t(rows), cuuint32_t(BK)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(op.p), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 1 : 0;
+}
+
 // Launch the GEMM core and, when the plan splits K, the fixed-order reduction.
 // `ws` is the caller's workspace (>= p.ws_elems floats) or nullptr, in which
 // case a stream-ordered allocation is used.
@@ -397,6 +436,13 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
             own = true;
         }
         p.ws = ws;
+    }
+    {
+        int BM, BN, NT;
+        size_t smem;
+        cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, 0);
+        p.tma_on[0] = setup_tma(&p.tma[0], a, BM);
+        p.tma_on[1] = setup_tma(&p.tma[1], b, BN);
     }
     amsim_status s = (eb == 8 && p.mul == MUL_LUT)    ? launch_eb<8>(p, a, b, st)
                      : (eb == 16 && p.mul == MUL_LUT) ? launch_eb<16>(p, a, b, st)

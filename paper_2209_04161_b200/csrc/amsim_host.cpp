@@ -131,7 +131,7 @@ uint64_t amsim_launch_count(void) { return g_launches.load(); }
 
 amsim_status amsim_set_path_policy(int policy)
 {
-    if (policy < 0 || policy > 7) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 7]");
+    if (policy < 0 || policy > 15) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 15]");
     g_policy.store(policy);
     return AMSIM_OK;
 }

@@ -616,3 +616,31 @@ def test_exponent_cast_gemm_and_conv(am, luts, orc, e):
         assert_bits(_run_conv(am, lut, d, x, w, dy, "fwd"), orc.conv_fwd(od, cx, cw, "mitchell").c32, "fwd")
         assert_bits(_run_conv(am, lut, d, x, w, dy, "dgrad"), orc.conv_bwd_data(od, cdy, cw, "mitchell").c32, "dgrad")
         assert_bits(_run_conv(am, lut, d, x, w, dy, "wgrad"), orc.conv_bwd_filter(od, cx, cdy, "mitchell").c32, "wgrad")
+
+
+# ---------------------------------------------------------------------------
+# TMA-staged operand tiles (policy bit 3 forces cp.async everywhere)
+
+def test_tma_staging_equals_cp_async(am, luts, orc):
+    """Plain-box operand tiles (conv fwd weights, wgrad errors, GEMM B and
+    transposed-A) are loaded by TMA by default; the bits equal the all-cp.async
+    path and the oracle, including ragged M / N / K edges (TMA zero fill)."""
+    lut = luts("mbm")
+    A = inp.normal((133, 77), 111)
+    B = inp.normal((77, 204), 112)            # ldb = 204: 16-byte row pitch -> TMA eligible
+    At = np.ascontiguousarray(inp.normal((77, 132), 113))   # trans_a, lda = 132 -> TMA eligible A
+    shape = (3, 13, 11, 12, 40, 3, 3, 2, 1)
+    x, w, dy, OH, OW = _conv_tensors(shape, 114)
+    d = am.conv_desc(*shape)
+    outs = {}
+    for pol in (2, 10):
+        am.amsim_set_path_policy(pol)
+        try:
+            outs[pol] = [run_gemm(am, lut, A, B), run_gemm(am, lut, At, B, trans_a=True),
+                         _run_conv(am, lut, d, x, w, dy, "fwd"), _run_conv(am, lut, d, x, w, dy, "wgrad")]
+        finally:
+            am.amsim_set_path_policy(0)
+    for i in range(4):
+        assert_bits(outs[2][i], outs[10][i], f"part {i}")
+    assert_bits(outs[2][0], orc.gemm(A, B, "mbm", 7).c32, "gemm vs c32")
+    assert_bits(outs[2][1], orc.gemm(np.ascontiguousarray(At.T), B, "mbm", 7).c32, "gemm trans_a vs c32")
