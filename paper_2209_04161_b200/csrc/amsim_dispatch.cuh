@@ -149,7 +149,7 @@ static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int polic
     p.nsub = pr.nsub;
     int Kmax = 0;
     for (int s = 0; s < pr.nsub; s++) Kmax = std::max(Kmax, pr.K[s]);
-    const int min_chunk = 16 * BK;  // >= 16 k-tiles per split
+    const int min_chunk = 4 * BK;   // >= 4 k-tiles per split (small problems need the parallelism)
     const int max_sp = (policy & 2) ? 1 : std::max(1, std::min(pr.max_splits, Kmax / min_chunk));
     // cost units: one k-tile of one BM x BN tile
     const double tile_overhead = 2.0;
@@ -430,8 +430,8 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
     if (p.ws_elems > 0) {
         if (!ws) {
             void *q = nullptr;
-            amsim_status s = cuda_check(cudaMallocAsync(&q, size_t(p.ws_elems) * sizeof(float), st), "cudaMallocAsync");
-            if (s != AMSIM_OK) return set_error(AMSIM_ERR_NOMEM, amsim_last_error());
+            amsim_status s = scratch_alloc(&q, size_t(p.ws_elems) * sizeof(float), st);
+            if (s != AMSIM_OK) return s;
             ws = static_cast<float *>(q);
             own = true;
         }
@@ -455,7 +455,7 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
         count_launch();
         s = cuda_check(cudaGetLastError(), "splitk_reduce launch");
     }
-    if (own) cudaFreeAsync(ws, st);
+    if (own) scratch_free(ws, st);
     return s;
 }
 

@@ -54,6 +54,39 @@ static inline float compose(uint32_t sign, int E, uint32_t mant)
     return flt(sign | (uint32_t(E) << 23) | (mant & 0x7FFFFFu));
 }
 
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pools[kMaxDevices];
+
+amsim_status scratch_alloc(void **ptr, size_t bytes, cudaStream_t stream)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+        return set_error(AMSIM_ERR_UNSUPPORTED, "no CUDA device");
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> g(g_pool_mu);
+        if (!g_pools[dev]) {
+            cudaMemPoolProps props = {};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            if (cudaMemPoolCreate(&g_pools[dev], &props) != cudaSuccess)
+                return set_error(AMSIM_ERR_NOMEM, "cudaMemPoolCreate failed");
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool = g_pools[dev];
+    }
+    cudaError_t e = cudaMallocFromPoolAsync(ptr, bytes, pool, stream);
+    if (e != cudaSuccess) return set_error(AMSIM_ERR_NOMEM, std::string("scratch allocation: ") + cudaGetErrorString(e));
+    return AMSIM_OK;
+}
+
+void scratch_free(void *ptr, cudaStream_t stream)
+{
+    if (ptr) cudaFreeAsync(ptr, stream);
+}
+
 // Upload the table for the current device in layout `eb` (8, 16 or 32 bits).
 static amsim_status upload(amsim_lut *lut, int dev, int eb, DeviceTable &t)
 {

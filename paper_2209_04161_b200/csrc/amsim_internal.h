@@ -2,6 +2,8 @@
 // kernel side (amsim_dispatch.cuh and the amsim_*.cu entry points) of libamsim.  Not part of the ABI.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -49,5 +51,12 @@ void count_launch(uint64_t n = 1);
 
 int path_policy();
 int multiply_mode();
+
+// Stream-ordered scratch (split-K partials, small coefficient buffers) from the
+// library's own per-device memory pool, which keeps freed memory (release
+// threshold = max) so steady-state calls never return to the OS allocator and
+// the host application's default pool is untouched.  Capturable in CUDA graphs.
+amsim_status scratch_alloc(void **ptr, size_t bytes, cudaStream_t stream);
+void scratch_free(void *ptr, cudaStream_t stream);
 
 }  // namespace amsim

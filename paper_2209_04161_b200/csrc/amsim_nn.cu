@@ -457,7 +457,7 @@ amsim_status amsim_bn_fwd_infer(const float *x, int64_t P, int32_t C, const floa
         return set_error(AMSIM_ERR_INVALID_ARG, "amsim_bn_fwd_infer: null tensor");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     float *coef = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void **>(&coef), size_t(C) * 8 + 16, st) != cudaSuccess)
+    if (scratch_alloc(reinterpret_cast<void **>(&coef), size_t(C) * 8 + 16, st) != AMSIM_OK)
         return set_error(AMSIM_ERR_NOMEM, "amsim_bn_fwd_infer: scratch allocation");
     float *scale = coef, *shift = coef + ((C + 3) & ~3);
     bn_infer_coeffs<<<(C + 127) / 128, 128, 0, st>>>(C, gamma, beta, running_mean, running_var, eps, scale, shift);
@@ -467,7 +467,7 @@ amsim_status amsim_bn_fwd_infer(const float *x, int64_t P, int32_t C, const floa
         bn_apply<4><<<grid_for(n / 4), NT, 0, st>>>(x, n, C, scale, shift, res, relu, y);
     else
         bn_apply<1><<<grid_for(n), NT, 0, st>>>(x, n, C, scale, shift, res, relu, y);
-    cudaFreeAsync(coef, st);
+    scratch_free(coef, st);
     count_launch(2);
     return check_launch("amsim_bn_fwd_infer");
 }

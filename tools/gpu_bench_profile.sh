@@ -6,7 +6,7 @@ timeout 900 python bench.py > gpurun_out/bench.jsonl 2> gpurun_out/bench.err
 tail -2 gpurun_out/bench.err
 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_ncu.log 2>&1
+    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-full-step > gpurun_out/bench_ncu.log 2>&1
 tail -2 gpurun_out/bench_ncu.log
 mkdir -p /tmp/reps
 for LP in "l3.1.conv2 fwd" "l1.0.conv2 fwd" "l3.1.conv2 wgrad" "l3.1.conv2 dgrad"; do

@@ -53,16 +53,20 @@ def main():
                 A = gen.normal((n, n), 1, device=dev)
                 B = gen.normal((n, n), 2, device=dev)
                 C = torch.empty((n, n), device=dev)
-                reps = max(1, min(args.reps, int(2 * 4096 ** 3 / n ** 3) + 1))
-                am.amsim_gemm(lut, A, B, C)          # warm-up (table upload, plan)
+                # per-repetition CUDA events, median reported (single slow reps -- allocator,
+                # clock transitions -- do not move it); more reps for the short problems
+                reps = max(3, min(50, int(20 * 1024 ** 3 / n ** 3) + 3))
+                for _ in range(2):
+                    am.amsim_gemm(lut, A, B, C)      # warm-up (table upload, plan)
                 torch.cuda.synchronize()
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                ev[0].record()
-                for _ in range(reps):
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+                for i in range(reps):
+                    ev[2 * i].record()
                     am.amsim_gemm(lut, A, B, C)
-                ev[1].record()
+                    ev[2 * i + 1].record()
                 torch.cuda.synchronize()
-                ms = ev[0].elapsed_time(ev[1]) / reps
+                ts = sorted(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(reps))
+                ms = ts[len(ts) // 2]
                 gmacs = n ** 3 / (ms * 1e-3) / 1e9
                 peak = sms * 32 * 1965e6 / 1e9
                 am.amsim_set_multiply_mode(0)
@@ -70,7 +74,7 @@ def main():
                                   "ms": ms, "gmacs": gmacs, "frac_of_32_lookups_per_clk": gmacs / peak,
                                   "lookup_measured_gps": lookup,
                                   "frac_of_measured_lookup": gmacs / lookup if lookup else None,
-                                  "reps": reps}), flush=True)
+                                  "reps": reps, "ms_min": ts[0], "ms_max": ts[-1]}), flush=True)
                 del A, B, C
                 torch.cuda.empty_cache()
 
