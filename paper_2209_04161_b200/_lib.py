@@ -219,19 +219,31 @@ def amsim_lut_build(model, m: int) -> Lut:
 # ---------------------------------------------------------------------------
 # compute entry points over torch CUDA tensors (device memory, current stream)
 
+_torch = None
+
+
+def _T():
+    global _torch
+    if _torch is None:
+        import torch
+        _torch = torch
+    return _torch
+
+
 def _stream(stream):
-    import torch
+    """cudaStream_t of `stream` (default: PyTorch's current stream on the current device)."""
     if stream is None:
-        stream = torch.cuda.current_stream()
-    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        torch = _T()
+        return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
 def _dptr(t, name):
     if t is None:
         return None
-    if not t.is_cuda or t.dtype.__str__() != "torch.float32":
+    if not t.is_cuda or t.dtype is not _T().float32:
         raise TypeError(f"{name} must be a float32 CUDA tensor")
-    return ctypes.c_void_p(t.data_ptr())
+    return t.data_ptr()
 
 
 def amsim_gemm(lut: Lut, A, B, C, trans_a: bool = False, trans_b: bool = False, accumulate: bool = False,

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 #include <cstdio>
@@ -305,6 +306,14 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     } else {
         cands = {CfgId::Big, CfgId::Lean};
     }
+    if (const char *f = std::getenv("AMSIM_FORCE_CFG")) {   // tuning experiments only
+        int fc = std::atoi(f);
+        for (CfgId c : cands)
+            if (int(c) == fc) {
+                cands = {c};
+                break;
+            }
+    }
     double best = 1e300;
     KParams bestp = p;
     for (CfgId c : cands) {
@@ -339,8 +348,16 @@ static amsim_status launch_cfg(const KParams &p, const OpA &a, const OpB &b, cud
 {
     size_t smem = Cf::smem_bytes((GL || MUL != MUL_LUT) ? 0u : p.lut_bytes);
     auto kern = amsim_mm_kernel<Cf, EB, OpA, OpB, GL, MUL>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
+    // opt in to the full shared-memory carve-out once per instantiation and device
+    // (a launch may then use any size up to it); per-call attribute setting cost ~us
+    static std::atomic<uint64_t> opted{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(opted.load(std::memory_order_relaxed) & (1ull << (dev & 63)))) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax));
+        if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
+        opted.fetch_or(1ull << (dev & 63));
+    }
     int grid = std::min(p.ntiles, num_sms());
     if (grid <= 0) return AMSIM_OK;
     kern<<<grid, Cf::NT, smem, st>>>(p, a, b);
