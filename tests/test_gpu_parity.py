@@ -441,10 +441,13 @@ def _lenet(am, lut, orc, model):
 FULL_LAYERS = ["stem", "l1.0.conv2", "l2.0.conv2", "l2.0.down", "l4.0.conv2", "l4.2.conv3"]
 
 
-@pytest.mark.parametrize("name", FULL_LAYERS)
-def test_resnet50_full_size_sampled(am, luts, orc, name):
-    """ResNet-50 b256 layers at full size in the bench's launch configuration;
-    the oracle recomputes sampled output rows one by one."""
+@pytest.mark.parametrize("name,model", [(n, "mbm") for n in FULL_LAYERS] +
+                         [(n, "exact") for n in FULL_LAYERS[:3]] + [("l3.1.conv2", "mitchell")])
+def test_resnet50_full_size_sampled(am, luts, orc, name, model):
+    """ResNet-50 b256 layers at full size in the bench's launch configuration
+    (the bench's MBM table: 16-bit packed path, TMA weight / error tiles, the
+    planner's tile shapes and split-K); the oracle recomputes sampled output
+    rows one by one."""
     import torch
     L = {l.name: l for l in inp.resnet50_layers(256)}[name]
     shape = (L.N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad)
@@ -454,10 +457,10 @@ def test_resnet50_full_size_sampled(am, luts, orc, name):
     x = inp.relu_normal((L.N, L.H, L.W, L.C), 1000)
     w = inp.he_normal((L.R, L.S, L.C, L.K), L.R * L.S * L.C, 1001)
     dy = inp.normal((L.N, L.OH, L.OW, L.K), 1002, 2 ** -10)
-    lut = luts("exact")
+    lut = luts(model)
     y = _run_conv(am, lut, d, x, w, dy, "fwd")
     rows = np.unique(np.concatenate([[0, y.shape[0] - 1], g.integers(0, y.shape[0], 14)]))
-    res = orc.conv_fwd(od, x, w, "exact", rows=rows)
+    res = orc.conv_fwd(od, x, w, model, rows=rows)
     assert_tol(y[rows], res, f"{name} fwd")
     with exact_order(am):
         y = _run_conv(am, lut, d, x, w, dy, "fwd")
@@ -465,11 +468,11 @@ def test_resnet50_full_size_sampled(am, luts, orc, name):
     if not L.first:
         dx = _run_conv(am, lut, d, x, w, dy, "dgrad")
         rows = np.unique(np.concatenate([[0, dx.shape[0] - 1], g.integers(0, dx.shape[0], 14)]))
-        res = orc.conv_bwd_data(od, dy, w, "exact", rows=rows)
+        res = orc.conv_bwd_data(od, dy, w, model, rows=rows)
         assert_tol(dx[rows], res, f"{name} dgrad")
     dw = _run_conv(am, lut, d, x, w, dy, "wgrad")
     rows = np.unique(np.concatenate([[0, dw.shape[0] - 1], g.integers(0, dw.shape[0], 6)]))
-    res = orc.conv_bwd_filter(od, x, dy, "exact", rows=rows)
+    res = orc.conv_bwd_filter(od, x, dy, model, rows=rows)
     assert_tol(dw[rows], res, f"{name} wgrad")
     torch.cuda.empty_cache()
 
