@@ -198,6 +198,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--policy", type=int, default=0, help="amsim_set_path_policy bits (A/B experiments only)")
     ap.add_argument("--no-full-step", action="store_true",
                     help="skip the whole-network training / inference step measurement (net.py)")
     ap.add_argument("--graph", action="store_true",
@@ -239,6 +240,7 @@ def main():
     _, nb = shard_batch(gb, world, rank)
     layers, _ = workload_layers(args.workload, nb)
     lut = am.Lut.build(args.model, args.m)
+    am.amsim_set_path_policy(args.policy)
     step = TrainStep(layers, lut, device=dev, seed=1000, first_input="mnist" if args.workload == "lenet5" else "relu")
     torch.cuda.synchronize()
 

@@ -82,6 +82,21 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, uint32_t bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ float lds_f32(uint32_t addr)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem()
 {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -173,14 +188,15 @@ struct SubP {
 };
 
 struct OpDesc {
-    int kcontig;          // raw tile stored [mn][BK + RAW_PAD] (k contiguous) or [BK][BMN]
+    int kcontig;          // raw tile stored [mn][BK + RAW_PAD] (k contiguous, 1), [BK][BMN] (0), or
+                          // [mn][BK] with TMA's 64-byte swizzle (k contiguous, TMA-loaded, 2)
     int vec_log2;         // 0 (4-byte copies) or 2 (16-byte copies along the contiguous dim)
 };
 
 struct KParams {
-    // TMA descriptors of the operands whose smem tile is a plain 2-D box of a
-    // row-major matrix ([BK][rows], rows contiguous: GemmOp with k strided),
-    // tma_on[0] = A, [1] = B; the other operands are gathered with cp.async.
+    // TMA descriptors of the operands whose smem tile is a box of a tensor
+    // (tma_on[0] = A, [1] = B: 0 = gathered with cp.async, 2 / 3 = 2-D / 3-D
+    // box at the coordinates the operand map's tma_coords() gives).
     CUtensorMap tma[2];
     int tma_on[2];
     int N, tiles_n, nsub, ntiles;
@@ -218,6 +234,13 @@ struct GemmOp {
         return kcontig ? p + int64_t(mn) * ld + k : p + int64_t(k) * ld + mn;
     }
     __device__ __forceinline__ int64_t out_row(int, int row, int64_t ldc) const { return int64_t(row) * ldc; }
+    // TMA box origin (innermost coordinate first): [k][mn] with mn contiguous, or [mn][k]
+    __device__ __forceinline__ void tma_coords(int, int mn0, int k0, int *c) const
+    {
+        c[0] = kcontig ? k0 : mn0;
+        c[1] = kcontig ? mn0 : k0;
+        c[2] = 0;
+    }
 };
 
 struct ConvGeom {
@@ -242,6 +265,13 @@ struct FwdX {
         return x + ((int64_t(n) * g.H + ih) * g.W + iw) * g.C + ci;
     }
     __device__ __forceinline__ int64_t out_row(int, int row, int64_t ldc) const { return int64_t(row) * ldc; }
+    // TMA (1x1, stride 1, no padding only): IM2COL(x) is x viewed as [pixels][C]
+    __device__ __forceinline__ void tma_coords(int, int m0, int k0, int *c) const
+    {
+        c[0] = k0;
+        c[1] = m0;
+        c[2] = 0;
+    }
 };
 
 // wgrad A: element (mn = (kh,kw,ci), k = (n,oh,ow)) = x[n][oh*s-p+kh][ow*s-p+kw][ci]
@@ -262,6 +292,13 @@ struct WgX {
         return x + ((int64_t(n) * g.H + ih) * g.W + iw) * g.C + ci;
     }
     __device__ __forceinline__ int64_t out_row(int, int row, int64_t ldc) const { return int64_t(row) * ldc; }
+    // TMA (1x1, stride 1, no padding only): element (ci, pixel) of x viewed as [pixels][C]
+    __device__ __forceinline__ void tma_coords(int, int mn0, int k0, int *c) const
+    {
+        c[0] = mn0;
+        c[1] = k0;
+        c[2] = 0;
+    }
 };
 
 // dgrad, per stride phase (a, b) in [0,sh) x [0,sw): the output pixels
@@ -304,6 +341,13 @@ struct DgDY {
         int h = g.sh * int(u) + P.ch, w = g.sw * int(v) + P.cw;
         return ((int64_t(n) * g.H + h) * g.W + w) * ldc;
     }
+    // TMA (1x1, stride 1, no padding only: one phase, dx pixel = dy pixel): dy as [pixels][K]
+    __device__ __forceinline__ void tma_coords(int, int m0, int k0, int *c) const
+    {
+        c[0] = k0;
+        c[1] = m0;
+        c[2] = 0;
+    }
 };
 
 // dgrad B: reverse_transpose(w) restricted to the phase's taps:
@@ -321,6 +365,18 @@ struct DgW {
         uint32_t j = fK.div(r2), co = r2 - j * g.K;
         int kh = P.a + g.sh * (P.th - 1 - int(i)), kw = P.b + g.sw * (P.tw - 1 - int(j));
         return w + ((int64_t(kh) * g.S + kw) * g.C + ci) * g.K + co;
+    }
+    // TMA (K % BK == 0, so a k-tile lies inside one tap): box {co, ci, tap} of w
+    // viewed as [R*S][C][K]
+    __device__ __forceinline__ void tma_coords(int s, int ci0, int k0, int *c) const
+    {
+        const DgPhase &P = ph[s];
+        uint32_t i = P.fTwK.div(uint32_t(k0)), r2 = uint32_t(k0) - i * uint32_t(P.tw * g.K);
+        uint32_t j = fK.div(r2), co = r2 - j * g.K;
+        int kh = P.a + g.sh * (P.th - 1 - int(i)), kw = P.b + g.sw * (P.tw - 1 - int(j));
+        c[0] = int(co);
+        c[1] = ci0;
+        c[2] = kh * g.S + kw;
     }
 };
 
@@ -402,7 +458,13 @@ __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, ui
         const int e = e0 + threadIdx.x;
         if (total % NT == 0 || e < total) {
             const int kk = e / ROWS, i = e % ROWS;
-            float v = kcontig ? raw[i * (BK + RAW_PAD) + kk] : raw[kk * ROWS + i];
+            float v;
+            if (kcontig == 2) {  // TMA tile [ROWS][BK] with the 64-byte swizzle: 16-B chunk ^= address bits 8..7
+                uint32_t a = smem_u32(raw) + uint32_t(i * BK + kk) * 4u;
+                v = lds_f32(a ^ (((a >> 7) & 3u) << 4));
+            } else {
+                v = kcontig ? raw[i * (BK + RAW_PAD) + kk] : raw[kk * ROWS + i];
+            }
             uint32_t u = __float_as_uint(v);
             uint32_t ex = (u >> 23) & 0xFFu;
             if (ex != 0 && ex != 255 && (ex < elo || ex > ehi)) {  // exponent cast to (1, e, m), reading C23
@@ -557,8 +619,17 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     // last __syncthreads; order those reads before the async-proxy writes
                     fence_proxy_async_smem();
                     mbar_expect_tx(bar, (p.tma_on[0] ? BM * BK * 4 : 0) + (p.tma_on[1] ? BN * BK * 4 : 0));
-                    if (p.tma_on[0]) tma_load_2d(smem_u32(ra), &p.tma[0], IT.m0, k0, bar);
-                    if (p.tma_on[1]) tma_load_2d(smem_u32(rb), &p.tma[1], IT.n0, k0, bar);
+                    int c[3];
+                    if (p.tma_on[0]) {
+                        opa.tma_coords(IT.s, IT.m0, k0, c);
+                        if (p.tma_on[0] == 3) tma_load_3d(smem_u32(ra), &p.tma[0], c[0], c[1], c[2], bar);
+                        else tma_load_2d(smem_u32(ra), &p.tma[0], c[0], c[1], bar);
+                    }
+                    if (p.tma_on[1]) {
+                        opb.tma_coords(IT.s, IT.n0, k0, c);
+                        if (p.tma_on[1] == 3) tma_load_3d(smem_u32(rb), &p.tma[1], c[0], c[1], c[2], bar);
+                        else tma_load_2d(smem_u32(rb), &p.tma[1], c[0], c[1], bar);
+                    }
                 }
             }
             if (!p.tma_on[0]) issue_operand<NT, BM>(opa, p.da, ra, IT.s, IT.m0, k0, IT.ke, dummy);

@@ -419,22 +419,91 @@ static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn()
     return fn;
 }
 
-template <class Op>
-static int setup_tma(CUtensorMap *, const Op &, int) { return 0; }
-
-static int setup_tma(CUtensorMap *map, const GemmOp &op, int rows)
+// Encode a tensor map over FP32 `base` with `rank` dims (innermost first),
+// byte strides of dims 1.., box `box`; kcontig tiles use the 64-byte swizzle
+// (the decode applies the same XOR).  Returns the TMA mode (2 / 3 = 2-D / 3-D)
+// or 0 when the tensor cannot be described (alignment) -> cp.async.
+static int encode_tma(CUtensorMap *map, const float *base, int rank, const cuuint64_t *dims,
+                      const cuuint64_t *strides, const cuuint32_t *box, bool swizzle)
 {
-    if (op.kcontig || (path_policy() & 8)) return 0;   // policy bit 3: cp.async for every operand
     auto fn = tma_encode_fn();
-    if (!fn || (reinterpret_cast<uintptr_t>(op.p) & 15) || (op.ld * 4) % 16 || op.MN <= 0 || op.K <= 0) return 0;
-    cuuint64_t dims[2] = {cuuint64_t(op.MN), cuuint64_t(op.K)};
-    cuuint64_t strides[1] = {cuuint64_t(op.ld) * 4};
+    if (!fn || (reinterpret_cast<uintptr_t>(base) & 15)) return 0;
+    for (int d = 0; d < rank; d++)
+        if (dims[d] == 0 || (d > 0 && strides[d - 1] % 16)) return 0;
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cuuint32_t(rank), const_cast<float *>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    swizzle ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? rank : 0;
+}
+
+static bool tma_disabled() { return (path_policy() & 8) != 0; }   // policy bit 3: cp.async for every operand
+
+// A row-major matrix (GemmOp): [k][mn] (mn contiguous) or [mn][k] (k contiguous, swizzled).
+static int setup_tma(CUtensorMap *map, const GemmOp &op, int rows, OpDesc &d)
+{
+    if (tma_disabled() || op.MN <= 0 || op.K <= 0) return 0;
+    cuuint64_t st[1] = {cuuint64_t(op.ld) * 4};
+    if (!op.kcontig) {
+        cuuint64_t dims[2] = {cuuint64_t(op.MN), cuuint64_t(op.K)};
+        cuuint32_t box[2] = {cuuint32_t(rows), cuuint32_t(BK)};
+        return encode_tma(map, op.p, 2, dims, st, box, false);
+    }
+    cuuint64_t dims[2] = {cuuint64_t(op.K), cuuint64_t(op.MN)};
+    cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(rows)};
+    int m = encode_tma(map, op.p, 2, dims, st, box, true);
+    if (m) d.kcontig = 2;
+    return m;
+}
+
+static bool is_1x1_s1(const ConvGeom &g) { return g.R == 1 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0; }
+
+// conv fwd A: for a 1x1 / stride-1 / unpadded conv, IM2COL(x) is x as [pixels][C]
+static int setup_tma(CUtensorMap *map, const FwdX &op, int rows, OpDesc &d)
+{
+    if (tma_disabled() || !is_1x1_s1(op.g)) return 0;
+    cuuint64_t dims[2] = {cuuint64_t(op.g.C), cuuint64_t(op.M)};
+    cuuint64_t st[1] = {cuuint64_t(op.g.C) * 4};
+    cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(rows)};
+    int m = encode_tma(map, op.x, 2, dims, st, box, true);
+    if (m) d.kcontig = 2;
+    return m;
+}
+
+// conv wgrad A: for 1x1 / stride 1 / unpadded, element (ci, pixel) of x as [pixels][C]
+static int setup_tma(CUtensorMap *map, const WgX &op, int rows, OpDesc &)
+{
+    if (tma_disabled() || !is_1x1_s1(op.g)) return 0;
+    cuuint64_t dims[2] = {cuuint64_t(op.g.C), cuuint64_t(op.Kd)};
+    cuuint64_t st[1] = {cuuint64_t(op.g.C) * 4};
     cuuint32_t box[2] = {cuuint32_t(rows), cuuint32_t(BK)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(op.p), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? 1 : 0;
+    return encode_tma(map, op.x, 2, dims, st, box, false);
+}
+
+// conv dgrad A: for 1x1 / stride 1 / unpadded (one phase), dy as [pixels][K]
+static int setup_tma(CUtensorMap *map, const DgDY &op, int rows, OpDesc &d)
+{
+    if (tma_disabled() || !is_1x1_s1(op.g)) return 0;
+    cuuint64_t dims[2] = {cuuint64_t(op.g.K), cuuint64_t(int64_t(op.g.N) * op.g.OH * op.g.OW)};
+    cuuint64_t st[1] = {cuuint64_t(op.g.K) * 4};
+    cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(rows)};
+    int m = encode_tma(map, op.dy, 2, dims, st, box, true);
+    if (m) d.kcontig = 2;
+    return m;
+}
+
+// conv dgrad B: the reverse-transposed weight taps, a 3-D box {co, ci, tap} of w
+// as [R*S][C][K] when every k-tile lies inside one tap (K % BK == 0)
+static int setup_tma(CUtensorMap *map, const DgW &op, int rows, OpDesc &d)
+{
+    if (tma_disabled() || op.g.K % BK) return 0;
+    cuuint64_t dims[3] = {cuuint64_t(op.g.K), cuuint64_t(op.g.C), cuuint64_t(op.g.R) * op.g.S};
+    cuuint64_t st[2] = {cuuint64_t(op.g.K) * 4, cuuint64_t(op.g.C) * op.g.K * 4};
+    cuuint32_t box[3] = {cuuint32_t(BK), cuuint32_t(rows), 1};
+    int m = encode_tma(map, op.w, 3, dims, st, box, true);
+    if (m) d.kcontig = 2;
+    return m;
 }
 
 // Launch the GEMM core and, when the plan splits K, the fixed-order reduction.
@@ -458,8 +527,8 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
         int BM, BN, NT;
         size_t smem;
         cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, 0);
-        p.tma_on[0] = setup_tma(&p.tma[0], a, BM);
-        p.tma_on[1] = setup_tma(&p.tma[1], b, BN);
+        p.tma_on[0] = setup_tma(&p.tma[0], a, BM, p.da);
+        p.tma_on[1] = setup_tma(&p.tma[1], b, BN, p.db);
     }
     amsim_status s = (eb == 8 && p.mul == MUL_LUT)    ? launch_eb<8>(p, a, b, st)
                      : (eb == 16 && p.mul == MUL_LUT) ? launch_eb<16>(p, a, b, st)

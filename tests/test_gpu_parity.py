@@ -293,6 +293,10 @@ CONV = [
     (3, 9, 9, 12, 130, 1, 1, 2, 0),      # 1x1 stride-2 downsample
     (2, 20, 20, 3, 16, 7, 7, 2, 3),      # stem geometry
     (4, 28, 28, 1, 6, 5, 5, 1, 2),       # LeNet c1
+    (2, 7, 7, 16, 40, 1, 1, 1, 0),       # 1x1 stride 1: TMA-staged x (fwd, wgrad) and dy (dgrad)
+    (1, 5, 9, 20, 32, 1, 1, 1, 0),       # 1x1 stride 1, K % 16 == 0: TMA weight taps in dgrad too
+    (2, 9, 9, 8, 48, 3, 3, 1, 1),        # 3x3, K % 16 == 0: 3-D TMA weight taps in dgrad
+    (2, 6, 6, 6, 32, 1, 1, 1, 0),        # 1x1 stride 1 with C % 4 != 0: cp.async fallback
 ]
 
 
@@ -625,25 +629,29 @@ def test_exponent_cast_gemm_and_conv(am, luts, orc, e):
 # TMA-staged operand tiles (policy bit 3 forces cp.async everywhere)
 
 def test_tma_staging_equals_cp_async(am, luts, orc):
-    """Plain-box operand tiles (conv fwd weights, wgrad errors, GEMM B and
-    transposed-A) are loaded by TMA by default; the bits equal the all-cp.async
-    path and the oracle, including ragged M / N / K edges (TMA zero fill)."""
+    """Box-shaped operand tiles (GEMM A / B, conv fwd weights, wgrad errors,
+    dgrad weight taps via 3-D maps, 1x1 / stride-1 activations and errors,
+    64-byte swizzled where k is contiguous) are loaded by TMA by default; the
+    bits equal the all-cp.async path and the oracle, including ragged
+    M / N / K edges (TMA zero fill)."""
     lut = luts("mbm")
     A = inp.normal((133, 77), 111)
     B = inp.normal((77, 204), 112)            # ldb = 204: 16-byte row pitch -> TMA eligible
     At = np.ascontiguousarray(inp.normal((77, 132), 113))   # trans_a, lda = 132 -> TMA eligible A
-    shape = (3, 13, 11, 12, 40, 3, 3, 2, 1)
-    x, w, dy, OH, OW = _conv_tensors(shape, 114)
-    d = am.conv_desc(*shape)
+    shapes = [(3, 13, 11, 12, 40, 3, 3, 2, 1), (2, 9, 7, 16, 48, 1, 1, 1, 0), (2, 8, 8, 12, 32, 3, 3, 1, 1),
+              (2, 10, 10, 8, 64, 3, 3, 2, 1)]
     outs = {}
     for pol in (2, 10):
         am.amsim_set_path_policy(pol)
         try:
-            outs[pol] = [run_gemm(am, lut, A, B), run_gemm(am, lut, At, B, trans_a=True),
-                         _run_conv(am, lut, d, x, w, dy, "fwd"), _run_conv(am, lut, d, x, w, dy, "wgrad")]
+            outs[pol] = [run_gemm(am, lut, A, B), run_gemm(am, lut, At, B, trans_a=True)]
+            for k, shape in enumerate(shapes):
+                x, w, dy, OH, OW = _conv_tensors(shape, 114 + k)
+                d = am.conv_desc(*shape)
+                outs[pol] += [_run_conv(am, lut, d, x, w, dy, which) for which in ("fwd", "wgrad", "dgrad")]
         finally:
             am.amsim_set_path_policy(0)
-    for i in range(4):
+    for i in range(len(outs[2])):
         assert_bits(outs[2][i], outs[10][i], f"part {i}")
     assert_bits(outs[2][0], orc.gemm(A, B, "mbm", 7).c32, "gemm vs c32")
     assert_bits(outs[2][1], orc.gemm(np.ascontiguousarray(At.T), B, "mbm", 7).c32, "gemm trans_a vs c32")
