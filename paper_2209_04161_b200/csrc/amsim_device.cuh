@@ -90,6 +90,19 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
+// im2col-mode TMA: pixelsPerColumn output pixels traversed from (w, h, n), each
+// reading channelsPerPixel channels from c at the tap offset (offw, offh)
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const CUtensorMap *map, int c, int w, int h, int n,
+                                                   int offw, int offh, uint32_t bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6], {%7, %8};\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar), "h"(uint16_t(offw)),
+        "h"(uint16_t(offh))
+        : "memory");
+}
+
 __device__ __forceinline__ float lds_f32(uint32_t addr)
 {
     float v;
@@ -196,7 +209,8 @@ struct OpDesc {
 struct KParams {
     // TMA descriptors of the operands whose smem tile is a box of a tensor
     // (tma_on[0] = A, [1] = B: 0 = gathered with cp.async, 2 / 3 = 2-D / 3-D
-    // box at the coordinates the operand map's tma_coords() gives).
+    // box, 4 = 4-D im2col box, at the coordinates the operand map's
+    // tma_coords() gives).
     CUtensorMap tma[2];
     int tma_on[2];
     int N, tiles_n, nsub, ntiles;
@@ -265,12 +279,28 @@ struct FwdX {
         return x + ((int64_t(n) * g.H + ih) * g.W + iw) * g.C + ci;
     }
     __device__ __forceinline__ int64_t out_row(int, int row, int64_t ldc) const { return int64_t(row) * ldc; }
-    // TMA (1x1, stride 1, no padding only): IM2COL(x) is x viewed as [pixels][C]
+    // TMA box origin.  1x1 / stride 1 / unpadded: IM2COL(x) is x viewed as
+    // [pixels][C] (2-D).  Otherwise im2col mode (C % BK == 0): the tile's first
+    // output pixel (n, oh, ow) gives the base (ow*sw - pw, oh*sh - ph, n), the
+    // k-tile's tap (kh, kw) the offsets, its channel chunk c.
     __device__ __forceinline__ void tma_coords(int, int m0, int k0, int *c) const
     {
-        c[0] = k0;
-        c[1] = m0;
-        c[2] = 0;
+        if (g.R == 1 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0) {
+            c[0] = k0;
+            c[1] = m0;
+            c[2] = 0;
+            return;
+        }
+        uint32_t n = g.fOHOW.div(uint32_t(m0)), r = uint32_t(m0) - n * uint32_t(g.OH * g.OW);
+        uint32_t oh = g.fOW.div(r), ow = r - oh * g.OW;
+        uint32_t kh = g.fSC.div(uint32_t(k0)), r2 = uint32_t(k0) - kh * uint32_t(g.S * g.C);
+        uint32_t kw = g.fC.div(r2), ci = r2 - kw * g.C;
+        c[0] = int(ci);
+        c[1] = int(ow) * g.sw - g.pw;
+        c[2] = int(oh) * g.sh - g.ph;
+        c[3] = int(n);
+        c[4] = int(kw);
+        c[5] = int(kh);
     }
 };
 
@@ -292,12 +322,28 @@ struct WgX {
         return x + ((int64_t(n) * g.H + ih) * g.W + iw) * g.C + ci;
     }
     __device__ __forceinline__ int64_t out_row(int, int row, int64_t ldc) const { return int64_t(row) * ldc; }
-    // TMA (1x1, stride 1, no padding only): element (ci, pixel) of x viewed as [pixels][C]
+    // TMA box origin.  1x1 / stride 1 / unpadded: element (ci, pixel) of x as
+    // [pixels][C] (2-D).  Otherwise im2col mode (C % BM == 0, so a row tile lies
+    // in one tap): BK output pixels from the k-tile's first (n, oh, ow), BM
+    // channels from the row tile's (kh, kw, ci0) -- smem [BK][BM].
     __device__ __forceinline__ void tma_coords(int, int mn0, int k0, int *c) const
     {
-        c[0] = mn0;
-        c[1] = k0;
-        c[2] = 0;
+        if (g.R == 1 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0) {
+            c[0] = mn0;
+            c[1] = k0;
+            c[2] = 0;
+            return;
+        }
+        uint32_t kh = g.fSC.div(uint32_t(mn0)), r2 = uint32_t(mn0) - kh * uint32_t(g.S * g.C);
+        uint32_t kw = g.fC.div(r2), ci = r2 - kw * g.C;
+        uint32_t n = g.fOHOW.div(uint32_t(k0)), r = uint32_t(k0) - n * uint32_t(g.OH * g.OW);
+        uint32_t oh = g.fOW.div(r), ow = r - oh * g.OW;
+        c[0] = int(ci);
+        c[1] = int(ow) * g.sw - g.pw;
+        c[2] = int(oh) * g.sh - g.ph;
+        c[3] = int(n);
+        c[4] = int(kw);
+        c[5] = int(kh);
     }
 };
 
@@ -341,12 +387,29 @@ struct DgDY {
         int h = g.sh * int(u) + P.ch, w = g.sw * int(v) + P.cw;
         return ((int64_t(n) * g.H + h) * g.W + w) * ldc;
     }
-    // TMA (1x1, stride 1, no padding only: one phase, dx pixel = dy pixel): dy as [pixels][K]
-    __device__ __forceinline__ void tma_coords(int, int m0, int k0, int *c) const
+    // TMA box origin (stride 1 only: one phase).  1x1 unpadded: dy as
+    // [pixels][K].  Otherwise im2col mode over dy (K % BK == 0): output pixel
+    // (n, h, w) has base (w + pw - (S-1), h + ph - (R-1), n) and tap (i, j) of the
+    // reverse_transpose order reads dy[h + ph - kh] with kh = R-1-i: offsets (j, i).
+    __device__ __forceinline__ void tma_coords(int s, int m0, int k0, int *c) const
     {
-        c[0] = k0;
-        c[1] = m0;
-        c[2] = 0;
+        if (g.R == 1 && g.S == 1 && g.ph == 0 && g.pw == 0) {
+            c[0] = k0;
+            c[1] = m0;
+            c[2] = 0;
+            return;
+        }
+        const DgPhase &P = ph[s];
+        uint32_t n = P.fHpWp.div(uint32_t(m0)), r = uint32_t(m0) - n * uint32_t(P.Hp * P.Wp);
+        uint32_t h = P.fWp.div(r), w = r - h * P.Wp;
+        uint32_t i = P.fTwK.div(uint32_t(k0)), r2 = uint32_t(k0) - i * uint32_t(P.tw * g.K);
+        uint32_t j = fK.div(r2), co = r2 - j * g.K;
+        c[0] = int(co);
+        c[1] = int(w) + g.pw - (g.S - 1);
+        c[2] = int(h) + g.ph - (g.R - 1);
+        c[3] = int(n);
+        c[4] = int(j);
+        c[5] = int(i);
     }
 };
 
@@ -619,10 +682,12 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     // last __syncthreads; order those reads before the async-proxy writes
                     fence_proxy_async_smem();
                     mbar_expect_tx(bar, (p.tma_on[0] ? BM * BK * 4 : 0) + (p.tma_on[1] ? BN * BK * 4 : 0));
-                    int c[3];
+                    int c[6];
                     if (p.tma_on[0]) {
                         opa.tma_coords(IT.s, IT.m0, k0, c);
-                        if (p.tma_on[0] == 3) tma_load_3d(smem_u32(ra), &p.tma[0], c[0], c[1], c[2], bar);
+                        if (p.tma_on[0] == 4)
+                            tma_load_im2col_4d(smem_u32(ra), &p.tma[0], c[0], c[1], c[2], c[3], c[4], c[5], bar);
+                        else if (p.tma_on[0] == 3) tma_load_3d(smem_u32(ra), &p.tma[0], c[0], c[1], c[2], bar);
                         else tma_load_2d(smem_u32(ra), &p.tma[0], c[0], c[1], bar);
                     }
                     if (p.tma_on[1]) {

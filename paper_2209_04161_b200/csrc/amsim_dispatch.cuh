@@ -440,6 +440,41 @@ static int encode_tma(CUtensorMap *map, const float *base, int rank, const cuuin
 
 static bool tma_disabled() { return (path_policy() & 8) != 0; }   // policy bit 3: cp.async for every operand
 
+static PFN_cuTensorMapEncodeIm2col_v12000 tma_im2col_fn()
+{
+    static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(f);
+    });
+    return fn;
+}
+
+// im2col-mode descriptor over an NHWC tensor [n][h][w][c]: `rows` pixels per
+// box (traversed w, h, n inside the bounding box [lower, dim - 1 + upper] with
+// the given traversal strides), BK channels per pixel, 64-byte swizzle.
+static int encode_im2col(CUtensorMap *map, const float *base, int N, int H, int W, int C, int lower_h, int lower_w,
+                         int upper_h, int upper_w, int sh, int sw, int rows, int chans = BK)
+{
+    auto fn = tma_im2col_fn();
+    if (!fn || (reinterpret_cast<uintptr_t>(base) & 15) || C % chans || N <= 0) return 0;
+    cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N)};
+    cuuint64_t st[3] = {cuuint64_t(C) * 4, cuuint64_t(W) * C * 4, cuuint64_t(H) * W * C * 4};
+    int lo[2] = {lower_w, lower_h}, hi[2] = {upper_w, upper_h};
+    cuuint32_t estr[4] = {1, cuuint32_t(sw), cuuint32_t(sh), 1};
+    // k-contiguous tiles (BK channels per pixel) use the 64-byte swizzle; wgrad's
+    // [BK pixels][BM channels] tiles are stored plainly
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(base), dims, st, lo, hi,
+                    cuuint32_t(chans), cuuint32_t(rows), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    chans == BK ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 4 : 0;
+}
+
 // A row-major matrix (GemmOp): [k][mn] (mn contiguous) or [mn][k] (k contiguous, swizzled).
 static int setup_tma(CUtensorMap *map, const GemmOp &op, int rows, OpDesc &d)
 {
@@ -459,10 +494,19 @@ static int setup_tma(CUtensorMap *map, const GemmOp &op, int rows, OpDesc &d)
 
 static bool is_1x1_s1(const ConvGeom &g) { return g.R == 1 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0; }
 
-// conv fwd A: for a 1x1 / stride-1 / unpadded conv, IM2COL(x) is x as [pixels][C]
+// conv fwd A: for a 1x1 / stride-1 / unpadded conv, IM2COL(x) is x as [pixels][C];
+// otherwise TMA's im2col mode (bounding box lower = -pad, upper = pad - (R-1),
+// traversal stride = conv stride) when C % BK == 0
 static int setup_tma(CUtensorMap *map, const FwdX &op, int rows, OpDesc &d)
 {
-    if (tma_disabled() || !is_1x1_s1(op.g)) return 0;
+    if (tma_disabled()) return 0;
+    if (!is_1x1_s1(op.g)) {
+        const ConvGeom &g = op.g;
+        int m = encode_im2col(map, op.x, g.N, g.H, g.W, g.C, -g.ph, -g.pw, g.ph - (g.R - 1), g.pw - (g.S - 1), g.sh,
+                              g.sw, rows);
+        if (m) d.kcontig = 2;
+        return m;
+    }
     cuuint64_t dims[2] = {cuuint64_t(op.g.C), cuuint64_t(op.M)};
     cuuint64_t st[1] = {cuuint64_t(op.g.C) * 4};
     cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(rows)};
@@ -471,20 +515,37 @@ static int setup_tma(CUtensorMap *map, const FwdX &op, int rows, OpDesc &d)
     return m;
 }
 
-// conv wgrad A: for 1x1 / stride 1 / unpadded, element (ci, pixel) of x as [pixels][C]
+// conv wgrad A: for 1x1 / stride 1 / unpadded, element (ci, pixel) of x as [pixels][C];
+// otherwise im2col mode with BK pixels x `rows` channels per box when C % rows == 0
 static int setup_tma(CUtensorMap *map, const WgX &op, int rows, OpDesc &)
 {
-    if (tma_disabled() || !is_1x1_s1(op.g)) return 0;
+    if (tma_disabled()) return 0;
+    if (!is_1x1_s1(op.g)) {
+        const ConvGeom &g = op.g;
+        if (rows > 256) return 0;
+        return encode_im2col(map, op.x, g.N, g.H, g.W, g.C, -g.ph, -g.pw, g.ph - (g.R - 1), g.pw - (g.S - 1), g.sh,
+                             g.sw, BK, rows);
+    }
     cuuint64_t dims[2] = {cuuint64_t(op.g.C), cuuint64_t(op.Kd)};
     cuuint64_t st[1] = {cuuint64_t(op.g.C) * 4};
     cuuint32_t box[2] = {cuuint32_t(rows), cuuint32_t(BK)};
     return encode_tma(map, op.x, 2, dims, st, box, false);
 }
 
-// conv dgrad A: for 1x1 / stride 1 / unpadded (one phase), dy as [pixels][K]
+// conv dgrad A: for 1x1 / stride 1 / unpadded (one phase), dy as [pixels][K];
+// other stride-1 convs: im2col mode over dy (lower = pad - (R-1),
+// upper = pad - (R-1) + H - OH) when K % BK == 0
 static int setup_tma(CUtensorMap *map, const DgDY &op, int rows, OpDesc &d)
 {
-    if (tma_disabled() || !is_1x1_s1(op.g)) return 0;
+    if (tma_disabled()) return 0;
+    const ConvGeom &g = op.g;
+    if (!is_1x1_s1(op.g)) {
+        if (g.sh != 1 || g.sw != 1) return 0;
+        int m = encode_im2col(map, op.dy, g.N, g.OH, g.OW, g.K, g.ph - (g.R - 1), g.pw - (g.S - 1),
+                              g.ph - (g.R - 1) + g.H - g.OH, g.pw - (g.S - 1) + g.W - g.OW, 1, 1, rows);
+        if (m) d.kcontig = 2;
+        return m;
+    }
     cuuint64_t dims[2] = {cuuint64_t(op.g.K), cuuint64_t(int64_t(op.g.N) * op.g.OH * op.g.OW)};
     cuuint64_t st[1] = {cuuint64_t(op.g.K) * 4};
     cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(rows)};

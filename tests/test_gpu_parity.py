@@ -297,6 +297,13 @@ CONV = [
     (1, 5, 9, 20, 32, 1, 1, 1, 0),       # 1x1 stride 1, K % 16 == 0: TMA weight taps in dgrad too
     (2, 9, 9, 8, 48, 3, 3, 1, 1),        # 3x3, K % 16 == 0: 3-D TMA weight taps in dgrad
     (2, 6, 6, 6, 32, 1, 1, 1, 0),        # 1x1 stride 1 with C % 4 != 0: cp.async fallback
+    (2, 9, 9, 16, 32, 3, 3, 1, 1),       # C, K % 16 == 0: im2col-mode TMA for fwd x and stride-1 dgrad dy
+    (3, 12, 10, 16, 16, 5, 5, 1, 2),     # 5x5 pad 2 im2col, ragged pixel tiles across images
+    (2, 20, 20, 32, 16, 7, 7, 2, 3),     # 7x7 stride 2 im2col (traversal stride 2)
+    (2, 9, 11, 16, 32, 3, 1, 1, 0),      # R != S im2col
+    (2, 11, 11, 32, 48, 3, 3, 2, 0),     # stride 2 unpadded, (H - R) % S != 0
+    (2, 9, 9, 64, 32, 3, 3, 1, 1),       # C % 64 == 0: im2col TMA for the wgrad activations too
+    (1, 10, 10, 128, 64, 3, 3, 2, 1),    # C % 128 == 0, stride 2
 ]
 
 
@@ -639,7 +646,8 @@ def test_tma_staging_equals_cp_async(am, luts, orc):
     B = inp.normal((77, 204), 112)            # ldb = 204: 16-byte row pitch -> TMA eligible
     At = np.ascontiguousarray(inp.normal((77, 132), 113))   # trans_a, lda = 132 -> TMA eligible A
     shapes = [(3, 13, 11, 12, 40, 3, 3, 2, 1), (2, 9, 7, 16, 48, 1, 1, 1, 0), (2, 8, 8, 12, 32, 3, 3, 1, 1),
-              (2, 10, 10, 8, 64, 3, 3, 2, 1)]
+              (2, 10, 10, 8, 64, 3, 3, 2, 1), (3, 9, 9, 32, 48, 3, 3, 1, 1), (2, 15, 15, 16, 32, 3, 3, 2, 1),
+              (2, 9, 9, 128, 64, 3, 3, 1, 1), (2, 12, 12, 64, 128, 3, 3, 2, 1)]
     outs = {}
     for pol in (2, 10):
         am.amsim_set_path_policy(pol)
