@@ -37,6 +37,9 @@ namespace dev {
 #ifndef AMSIM_PACK
 #define AMSIM_PACK 1
 #endif
+#ifndef AMSIM_PACK8
+#define AMSIM_PACK8 0
+#endif
 
 constexpr int BK = 16;
 constexpr int STAGES = 3;
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // shared memory (global table offsets can exceed 23 bits; the 8-bit path is
     // issue-bound and loses more to the unpacking than it gains: measured
     // +5.7 % / -3.8 % on the ResNet-50 step)
-    constexpr bool PK = AMSIM_PACK && MUL == MUL_LUT && !GL && EB >= 16;
+    constexpr bool PK = AMSIM_PACK && MUL == MUL_LUT && !GL && (EB >= 16 || AMSIM_PACK8);
     constexpr uint32_t AMASK = 0xFF800000u, OMASK = 0x007FFFFFu;
     extern __shared__ __align__(128) unsigned char smem[];
 
