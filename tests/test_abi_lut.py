@@ -196,3 +196,28 @@ def test_exponent_bits_handle(built):
     for bad in (0, 9, -1):
         with pytest.raises(am.AmsimError):
             lut.with_exponent_bits(bad)
+
+
+def _build_example(tmp_path):
+    import subprocess
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    pkg = os.path.join(ROOT, "paper_2209_04161_b200")
+    exe = str(tmp_path / "amsim_example")
+    subprocess.run(["gcc", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(cuda, "include"),
+                    os.path.join(ROOT, "examples", "amsim_example.c"), "-L", pkg, "-lamsim",
+                    "-L", os.path.join(cuda, "lib64"), "-lcudart", "-lm", f"-Wl,-rpath,{pkg}", "-o", exe],
+                   check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_example_builds_against_the_abi(built, tmp_path):
+    """The ABI is usable from plain C (no Python / PyTorch): examples/amsim_example.c
+    compiles and links against libamsim.so + cudart."""
+    assert os.path.exists(_build_example(tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_example_runs(built, tmp_path):
+    import subprocess
+    r = subprocess.run([_build_example(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "amsim_example: ok" in r.stdout, r.stdout + r.stderr
