@@ -7,4 +7,4 @@ timeout 600 python tools/sweep.py --sizes 4096 --ms 7 9 11 --models mitchell exa
 timeout 900 python tools/paper_ratios.py > gpurun_out/ratios.jsonl 2> gpurun_out/ratios.err
 timeout 1200 python tools/full_step.py > gpurun_out/full_step.jsonl 2> gpurun_out/full_step.err
 timeout 300 python bench.py --model mitchell --no-cpu-baseline > gpurun_out/bench_mitchell.jsonl 2> gpurun_out/bench_mitchell.err
-tail -2 gpurun_out/*.err
+for f in gpurun_out/*.err; do tail -n 2 $f; done
