@@ -214,9 +214,12 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
  *   bit 2 -- use the 32-bit device table layout even when the table fits 8
  *            or 16 bits (tests: the layout changes speed, never bits);
  *   bit 3 -- stage every operand tile with cp.async gathers (default: tiles
- *            that are plain boxes of a row-major matrix -- the weights of conv
- *            fwd, the errors of wgrad, GEMM B -- are loaded by TMA).
- * Errors: AMSIM_ERR_INVALID_ARG outside [0, 15]. */
+ *            that are boxes of a tensor -- GEMM operands, conv weights, wgrad
+ *            errors, im2col boxes of activations / errors -- are loaded by TMA);
+ *   bit 4 -- never use the transposed kernel orientation (default: for a
+ *            symmetric table and N <= 128 << M the planner may make the
+ *            output channels the warp-shared rows; same bits).
+ * Errors: AMSIM_ERR_INVALID_ARG outside [0, 31]. */
 amsim_status amsim_set_path_policy(int policy);
 
 /* Multiply mode (process-wide, default AMSIM_MUL_LUT).  The two other modes

@@ -28,9 +28,9 @@ amsim_status amsim_conv2d_bwd_filter_workspace(const amsim_lut *lut, const amsim
     // The plan (hence the workspace) depends on the multiply mode and the
     // table layout policy; report the maximum so one allocation serves all.
     int64_t need = 0;
-    const int pol = path_policy() & 3;
+    const int pol = path_policy() & 3;   // bits 2 (table layout) and 4 (orientation) are varied below
     for (int mode : {AMSIM_MUL_LUT, AMSIM_MUL_NATIVE})
-        for (int policy : {pol, pol | 4}) {
+        for (int policy : {pol, pol | 4, pol | 16, pol | 4 | 16}) {
             KParams p{};
             ConvGeom g;
             int eb;

@@ -232,6 +232,7 @@ struct KParams {
     int lut_global;       // table read from global memory / L2 (too large for shared memory)
     int ecast_lo, ecast_hi;  // exponent casting (reading C23): normal exponent fields outside [lo, hi] -> 0 / Inf
     int mul;              // MulMode
+    int trn;              // transposed orientation (see amsim_mm_kernel)
 };
 
 // ---------------------------------------------------------------------------
@@ -586,7 +587,13 @@ __device__ __forceinline__ uint32_t direct_entry(uint32_t oa, uint32_t ob)
     }
 }
 
-template <class Cf, int EB, class OpA, class OpB, bool GL = false, int MUL = MUL_LUT>
+// TRN (transposed orientation): the kernel computes C^T = op(B)^T op(A)^T for
+// a skinny-N problem -- opa is the ORIGINAL B operand's map (its elements are
+// the warp-shared rows), opb the original A operand's (lanes), the table is
+// used transposed (only symmetric tables, so LUT^T = LUT), and the epilogue /
+// reduction write C[opb.out_row(col) + row]: each lane stores TM consecutive
+// output channels of one pixel (32-64 contiguous bytes).
+template <class Cf, int EB, class OpA, class OpB, bool GL = false, int MUL = MUL_LUT, bool TRN = false>
 __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_constant__ KParams p,
                                                              const __grid_constant__ OpA opa,
                                                              const __grid_constant__ OpB opb)
@@ -686,17 +693,18 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     fence_proxy_async_smem();
                     mbar_expect_tx(bar, (p.tma_on[0] ? BM * BK * 4 : 0) + (p.tma_on[1] ? BN * BK * 4 : 0));
                     int c[6];
+                    auto load = [&](int mode, const CUtensorMap *map, uint32_t dst) {
+                        if (mode == 4) tma_load_im2col_4d(dst, map, c[0], c[1], c[2], c[3], c[4], c[5], bar);
+                        else if (mode == 3) tma_load_3d(dst, map, c[0], c[1], c[2], bar);
+                        else tma_load_2d(dst, map, c[0], c[1], bar);
+                    };
                     if (p.tma_on[0]) {
                         opa.tma_coords(IT.s, IT.m0, k0, c);
-                        if (p.tma_on[0] == 4)
-                            tma_load_im2col_4d(smem_u32(ra), &p.tma[0], c[0], c[1], c[2], c[3], c[4], c[5], bar);
-                        else if (p.tma_on[0] == 3) tma_load_3d(smem_u32(ra), &p.tma[0], c[0], c[1], c[2], bar);
-                        else tma_load_2d(smem_u32(ra), &p.tma[0], c[0], c[1], bar);
+                        load(p.tma_on[0], &p.tma[0], smem_u32(ra));
                     }
                     if (p.tma_on[1]) {
                         opb.tma_coords(IT.s, IT.n0, k0, c);
-                        if (p.tma_on[1] == 3) tma_load_3d(smem_u32(rb), &p.tma[1], c[0], c[1], c[2], bar);
-                        else tma_load_2d(smem_u32(rb), &p.tma[1], c[0], c[1], bar);
+                        load(p.tma_on[1], &p.tma[1], smem_u32(rb));
                     }
                 }
             }
@@ -886,11 +894,38 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
         const SubP &S = p.sub[T.s];
         const bool split_out = S.splits > 1;
         float *Cb = split_out ? p.ws + S.ws_offset + int64_t(T.split) * S.M * p.N : p.C;
+        if constexpr (TRN) {
+            if (!split_out) {
+                const int row0 = T.m0 + warp * TM;
+#pragma unroll
+                for (int c = 0; c < TN; c++) {
+                    int col = T.n0 + lane * CG + Cf::col(c);
+                    if (col >= p.N) continue;
+                    float *dst = p.C + opb.out_row(T.s, col, p.ldc) + row0;
+                    if (row0 + TM <= S.M && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && !p.accumulate) {
+#pragma unroll
+                        for (int r = 0; r < TM; r += 4)
+                            *reinterpret_cast<float4 *>(dst + r) =
+                                make_float4(acc[r][c], acc[r + 1][c], acc[r + 2][c], acc[r + 3][c]);
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < TM; r++)
+                            if (row0 + r < S.M) dst[r] = p.accumulate ? dst[r] + acc[r][c] : acc[r][c];
+                    }
+                }
+                continue;
+            }
+        }
 #pragma unroll
         for (int r = 0; r < TM; r++) {
             int row = T.m0 + warp * TM + r;
             if (row >= S.M) continue;
-            float *dst = Cb + (split_out ? int64_t(row) * p.N : opa.out_row(T.s, row, p.ldc));
+            int64_t off;
+            if constexpr (TRN)
+                off = int64_t(row) * p.N;   // only split partials reach here in the transposed orientation
+            else
+                off = split_out ? int64_t(row) * p.N : opa.out_row(T.s, row, p.ldc);
+            float *dst = Cb + off;
 #pragma unroll
             for (int c = 0; c < TN; c++) {
                 int col = T.n0 + lane * CG + Cf::col(c);
@@ -902,8 +937,9 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 }
 
 // Deterministic split-K reduction for sub-problem blockIdx.y:
-// C[out_row(s, i)][j] (+)= sum over splits, in increasing split order.
-template <class OpA>
+// C[out_row(s, i)][j] (+)= sum over splits, in increasing split order
+// (TRN: C[out_row(s, j)][i], opa being the original A operand's map).
+template <class OpA, bool TRN = false>
 __global__ void splitk_reduce_kernel(const __grid_constant__ KParams p, const __grid_constant__ OpA opa)
 {
     const SubP &S = p.sub[blockIdx.y];
@@ -914,7 +950,7 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ KParams p, const __
         float s = 0.0f;
         for (int k = 0; k < S.splits; k++) s += ws[int64_t(k) * total + e];
         int i = int(e / p.N), j = int(e - int64_t(i) * p.N);
-        float *dst = p.C + opa.out_row(blockIdx.y, i, p.ldc) + j;
+        float *dst = TRN ? p.C + opa.out_row(blockIdx.y, j, p.ldc) + i : p.C + opa.out_row(blockIdx.y, i, p.ldc) + j;
         *dst = p.accumulate ? (*dst + s) : s;
     }
 }

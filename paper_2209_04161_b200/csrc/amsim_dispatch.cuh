@@ -237,7 +237,7 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
 // Plan cache: the same problem (shape, table width, mode, policy) is planned
 // once per process.
 struct PlanRec {
-    int cfg, tiles_n, nsub, ntiles;
+    int cfg, tiles_n, nsub, ntiles, trn;
     int64_t ws_elems;
     SubP sub[MAX_SUB];
 };
@@ -280,7 +280,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     p.policy = policy & 1;
     const bool smem_table = !p.lut_global && p.mul == MUL_LUT;
     const uint32_t smem_lut = smem_table ? bytes : 0u;
-    std::vector<int64_t> key = {pr.N, pr.nsub, pr.max_splits, eb, p.lut_global, p.mul, policy & 3, mbits,
+    std::vector<int64_t> key = {pr.N, pr.nsub, pr.max_splits, eb, p.lut_global, p.mul, policy & (3 | 16), mbits,
                                 num_sms()};
     for (int i = 0; i < pr.nsub; i++) {
         key.push_back(pr.M[i]);
@@ -291,7 +291,8 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         auto it = g_plans.find(key);
         if (it != g_plans.end()) {
             const PlanRec &r = it->second;
-            p.cfg = r.cfg; p.N = pr.N; p.tiles_n = r.tiles_n; p.nsub = r.nsub; p.ntiles = r.ntiles;
+            p.cfg = r.cfg; p.trn = r.trn; p.N = r.trn ? pr.M[0] : pr.N; p.tiles_n = r.tiles_n; p.nsub = r.nsub;
+            p.ntiles = r.ntiles;
             p.ws_elems = r.ws_elems; p.ws = nullptr;
             std::memcpy(p.sub, r.sub, sizeof(r.sub));
             return AMSIM_OK;
@@ -323,31 +324,57 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         if (smem > kSmemMax) continue;
         KParams q = p;
         q.cfg = int(c);
+        q.trn = 0;
         double cost = tile_plan(q, pr, BM, BN, policy) * double(BM) * BN * wf_per_lookup(c, eb, mbits, smem_table);
         if (cost < best * 0.999) {
             best = cost;
             bestp = q;
         }
     }
+    // Transposed orientation for skinny N (the output channels become the
+    // warp-shared rows, the pixels the lanes): symmetric shared-memory tables,
+    // one sub-problem, N well below M (policy bit 4 disables it).
+    if (smem_table && lut->symmetric && pr.nsub == 1 && eb <= 16 && pr.N <= 128 && pr.M[0] >= 4 * pr.N &&
+        !(policy & 16)) {
+        Problem pt = pr;
+        pt.N = pr.M[0];
+        pt.M[0] = pr.N;
+        std::vector<CfgId> tc = {CfgId::Wide, CfgId::Big};
+        if (eb >= 16) tc.push_back(CfgId::Huge);
+        for (CfgId c : tc) {
+            int BM, BN, NT;
+            size_t smem;
+            cfg_shape(c, BM, BN, NT, smem, smem_lut);
+            if (smem > kSmemMax) continue;
+            KParams q = p;
+            q.cfg = int(c);
+            q.trn = 1;
+            double cost = tile_plan(q, pt, BM, BN, policy) * double(BM) * BN * wf_per_lookup(c, eb, mbits, smem_table);
+            if (cost < best * 0.999) {
+                best = cost;
+                bestp = q;
+            }
+        }
+    }
     if (best >= 1e299) return set_error(AMSIM_ERR_UNSUPPORTED, "no tile configuration fits shared memory");
     p = bestp;
-    if (std::getenv("AMSIM_DEBUG_PLAN"))
-        std::fprintf(stderr, "[amsim plan] N=%d M0=%d K0=%d nsub=%d eb=%d mul=%d -> cfg=%d tiles=%d splits0=%d ws=%lld\n",
-                     pr.N, pr.M[0], pr.K[0], pr.nsub, eb, p.mul, p.cfg, p.ntiles, p.sub[0].splits,
+    if (const char *dbg = std::getenv("AMSIM_DEBUG_PLAN"); dbg && *dbg && *dbg != '0')
+        std::fprintf(stderr, "[amsim plan] N=%d M0=%d K0=%d nsub=%d eb=%d mul=%d -> cfg=%d trn=%d tiles=%d splits0=%d ws=%lld\n",
+                     pr.N, pr.M[0], pr.K[0], pr.nsub, eb, p.mul, p.cfg, p.trn, p.ntiles, p.sub[0].splits,
                      (long long)p.ws_elems);
     PlanRec r;
-    r.cfg = p.cfg; r.tiles_n = p.tiles_n; r.nsub = p.nsub; r.ntiles = p.ntiles; r.ws_elems = p.ws_elems;
+    r.cfg = p.cfg; r.trn = p.trn; r.tiles_n = p.tiles_n; r.nsub = p.nsub; r.ntiles = p.ntiles; r.ws_elems = p.ws_elems;
     std::memcpy(r.sub, p.sub, sizeof(r.sub));
     std::lock_guard<std::mutex> g(g_plan_mu);
     g_plans.emplace(std::move(key), r);
     return AMSIM_OK;
 }
 
-template <class Cf, int EB, class OpA, class OpB, bool GL = false, int MUL = MUL_LUT>
+template <class Cf, int EB, class OpA, class OpB, bool GL = false, int MUL = MUL_LUT, bool TRN = false>
 static amsim_status launch_cfg(const KParams &p, const OpA &a, const OpB &b, cudaStream_t st)
 {
     size_t smem = Cf::smem_bytes((GL || MUL != MUL_LUT) ? 0u : p.lut_bytes);
-    auto kern = amsim_mm_kernel<Cf, EB, OpA, OpB, GL, MUL>;
+    auto kern = amsim_mm_kernel<Cf, EB, OpA, OpB, GL, MUL, TRN>;
     // opt in to the full shared-memory carve-out once per instantiation and device
     // (a launch may then use any size up to it); per-call attribute setting cost ~us
     static std::atomic<uint64_t> opted{0};
@@ -567,6 +594,22 @@ static int setup_tma(CUtensorMap *map, const DgW &op, int rows, OpDesc &d)
     return m;
 }
 
+// Transposed orientation: the row operand is the original B (opr), the lanes'
+// the original A (opc); shared-memory tables of 8 / 16 bits only.
+template <int EB, class OpR, class OpC>
+static amsim_status launch_trn(const KParams &p, const OpR &r, const OpC &c, cudaStream_t st)
+{
+    switch (CfgId(p.cfg)) {
+    case CfgId::Wide: return launch_cfg<CfgWide, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
+    case CfgId::Big: return launch_cfg<CfgBig, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
+    case CfgId::Huge:
+        if constexpr (EB >= 16) return launch_cfg<CfgHuge, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
+        else break;
+    default: break;
+    }
+    return set_error(AMSIM_ERR_UNSUPPORTED, "internal: transposed orientation with this tile configuration");
+}
+
 // Launch the GEMM core and, when the plan splits K, the fixed-order reduction.
 // `ws` is the caller's workspace (>= p.ws_elems floats) or nullptr, in which
 // case a stream-ordered allocation is used.
@@ -584,21 +627,30 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
         }
         p.ws = ws;
     }
-    {
-        int BM, BN, NT;
-        size_t smem;
-        cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, 0);
+    int BM, BN, NT;
+    size_t smem;
+    cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, 0);
+    amsim_status s;
+    if (p.trn) {   // rows = original B operand, lanes = original A operand
+        std::swap(p.da, p.db);
+        p.tma_on[0] = setup_tma(&p.tma[0], b, BM, p.da);
+        p.tma_on[1] = setup_tma(&p.tma[1], a, BN, p.db);
+        s = eb == 8 ? launch_trn<8>(p, b, a, st) : launch_trn<16>(p, b, a, st);
+    } else {
         p.tma_on[0] = setup_tma(&p.tma[0], a, BM, p.da);
         p.tma_on[1] = setup_tma(&p.tma[1], b, BN, p.db);
+        s = (eb == 8 && p.mul == MUL_LUT)    ? launch_eb<8>(p, a, b, st)
+            : (eb == 16 && p.mul == MUL_LUT) ? launch_eb<16>(p, a, b, st)
+                                             : launch_eb<32>(p, a, b, st);
     }
-    amsim_status s = (eb == 8 && p.mul == MUL_LUT)    ? launch_eb<8>(p, a, b, st)
-                     : (eb == 16 && p.mul == MUL_LUT) ? launch_eb<16>(p, a, b, st)
-                                                      : launch_eb<32>(p, a, b, st);
     if (s == AMSIM_OK && p.ws_elems > 0) {
         int64_t maxmn = 0;
         for (int i = 0; i < p.nsub; i++) maxmn = std::max<int64_t>(maxmn, int64_t(p.sub[i].M) * p.N);
         int bx = int(std::max<int64_t>(1, std::min<int64_t>((maxmn + 255) / 256, 4L * num_sms())));
-        splitk_reduce_kernel<OpA><<<dim3(bx, p.nsub), 256, 0, st>>>(p, a);
+        if (p.trn)
+            splitk_reduce_kernel<OpA, true><<<dim3(bx, p.nsub), 256, 0, st>>>(p, a);
+        else
+            splitk_reduce_kernel<OpA><<<dim3(bx, p.nsub), 256, 0, st>>>(p, a);
         count_launch();
         s = cuda_check(cudaGetLastError(), "splitk_reduce launch");
     }

@@ -148,6 +148,16 @@ static void finalize_lut(amsim_lut *lut)
     uint32_t low = 0;
     for (uint32_t e : lut->entries) low |= e;
     lut->device_entry_bits = (low & 0xFFFFu) == 0 ? 8 : ((low & 0xFFu) == 0 ? 16 : 32);
+    // symmetric tables (model(a, b) == model(b, a) on every probe pair) may be used
+    // transposed, which the skinny-N kernel orientation needs
+    const size_t n = size_t(1) << lut->m;
+    lut->symmetric = true;
+    for (size_t k = 0; k < n && lut->symmetric; k++)
+        for (size_t j = k + 1; j < n; j++)
+            if (lut->entries[k * n + j] != lut->entries[j * n + k]) {
+                lut->symmetric = false;
+                break;
+            }
 }
 
 }  // namespace amsim
@@ -164,7 +174,7 @@ uint64_t amsim_launch_count(void) { return g_launches.load(); }
 
 amsim_status amsim_set_path_policy(int policy)
 {
-    if (policy < 0 || policy > 15) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 15]");
+    if (policy < 0 || policy > 31) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 31]");
     g_policy.store(policy);
     return AMSIM_OK;
 }
@@ -380,6 +390,7 @@ amsim_status amsim_lut_with_exponent_bits(const amsim_lut *src, int e_bits, amsi
     lut->entries = src->entries;
     lut->device_entry_bits = src->device_entry_bits;
     lut->model_id = src->model_id;
+    lut->symmetric = src->symmetric;
     lut->e_bits = e_bits;
     *out = lut;
     return AMSIM_OK;

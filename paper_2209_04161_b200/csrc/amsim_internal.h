@@ -29,6 +29,7 @@ struct DeviceTable {
 struct amsim_lut {
     int m = 0;
     std::vector<uint32_t> entries;   // Alg. 1 layout: (carry << 23) | mantissa
+    bool symmetric = false;          // entries[k][j] == entries[j][k] for all k, j
     int e_bits = 8;                  // operand exponent casting (1, e, m), reading C23
     int model_id = -1;               // built-in model the table was built from (0 exact, 1 Mitchell, 2 MBM), else -1
     int device_entry_bits = 32;      // 8 if every (e & 0xFFFF) == 0, else 16 if every (e & 0xFF) == 0

@@ -663,3 +663,36 @@ def test_tma_staging_equals_cp_async(am, luts, orc):
         assert_bits(outs[2][i], outs[10][i], f"part {i}")
     assert_bits(outs[2][0], orc.gemm(A, B, "mbm", 7).c32, "gemm vs c32")
     assert_bits(outs[2][1], orc.gemm(np.ascontiguousarray(At.T), B, "mbm", 7).c32, "gemm trans_a vs c32")
+
+
+# ---------------------------------------------------------------------------
+# transposed orientation for skinny N (policy bit 4 disables it)
+
+@pytest.mark.parametrize("model", ["mbm", "mitchell"])
+def test_transposed_orientation_equals_normal(am, luts, orc, model):
+    """For N <= 128 << M and a symmetric table the planner may make the output
+    channels the warp-shared rows (the kernel computes C^T, the epilogue and
+    split-K reduction write C transposed).  Same bits as the normal
+    orientation and as the oracle's sequential order."""
+    lut = luts(model)
+    A = inp.normal((1000, 300), 121)
+    B = inp.normal((300, 40), 122)
+    shapes = [(4, 16, 16, 16, 32, 3, 3, 1, 1), (2, 20, 20, 64, 64, 1, 1, 1, 0), (3, 14, 14, 32, 48, 3, 3, 2, 1),
+              (2, 12, 12, 128, 64, 3, 3, 1, 1)]
+    outs = {}
+    for pol in (2, 18, 0, 16):
+        am.amsim_set_path_policy(pol)
+        try:
+            outs[pol] = [run_gemm(am, lut, A, B), run_gemm(am, lut, np.ascontiguousarray(A.T), B, trans_a=True)]
+            for k, shape in enumerate(shapes):
+                x, w, dy, OH, OW = _conv_tensors(shape, 123 + k)
+                d = am.conv_desc(*shape)
+                outs[pol] += [_run_conv(am, lut, d, x, w, dy, which) for which in ("fwd", "wgrad", "dgrad")]
+        finally:
+            am.amsim_set_path_policy(0)
+    for i in range(len(outs[2])):
+        assert_bits(outs[2][i], outs[18][i], f"exact order, part {i}")
+    assert_bits(outs[2][0], orc.gemm(A, B, model, 7).c32, "gemm vs c32")
+    res = orc.gemm(A, B, model, 7)
+    assert_tol(outs[0][0], res, "gemm split")
+    assert_tol(outs[16][0], res, "gemm split, normal orientation")
