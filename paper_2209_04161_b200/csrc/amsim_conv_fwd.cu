@@ -19,6 +19,7 @@ amsim_status amsim_conv2d_fwd(const amsim_lut *lut, const amsim_conv2d_desc *d, 
     ConvGeom g;
     init_geom(g, d);
     Problem pr;
+    pr.a_is_activation = true;
     pr.N = d->K;
     pr.M[0] = d->N * g.OH * g.OW;
     pr.K[0] = d->R * d->S * d->C;

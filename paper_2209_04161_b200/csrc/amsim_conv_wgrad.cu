@@ -12,6 +12,7 @@ static amsim_status wgrad_plan(const amsim_lut *lut, const amsim_conv2d_desc *d,
 {
     init_geom(g, d);
     Problem pr;
+    pr.a_is_activation = true;
     pr.N = d->K;
     pr.M[0] = d->R * d->S * d->C;
     pr.K[0] = d->N * g.OH * g.OW;
@@ -57,9 +58,11 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
     s = wgrad_plan(lut, d, p, g, eb);
     if (s != AMSIM_OK) return s;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const SubP &S = p.sub[0];
-    if (S.K == 0) {
-        fill_zero_kernel<<<64, 256, 0, st>>>(dw, S.M, p.N, p.N);
+    // original problem dims (the plan's sub-problem / N are transposed when the
+    // planner picked the transposed orientation)
+    const int Mo = d->R * d->S * d->C, No = d->K, Ko = d->N * g.OH * g.OW;
+    if (Ko == 0) {
+        fill_zero_kernel<<<64, 256, 0, st>>>(dw, Mo, No, No);
         count_launch();
         return cuda_check(cudaGetLastError(), "fill_zero launch");
     }
@@ -67,12 +70,12 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
     if (need > 0 && (!workspace || workspace_bytes < need))
         return set_error(AMSIM_ERR_INVALID_ARG, "amsim_conv2d_bwd_filter: workspace too small (need " +
                                                     std::to_string(need) + " bytes)");
-    WgX a{x, g, S.M, S.K};
-    GemmOp b{dy, d->K, p.N, S.K, 0};
+    WgX a{x, g, Mo, Ko};
+    GemmOp b{dy, d->K, No, Ko, 0};
     p.da = OpDesc{0, (d->C % 4 == 0 && aligned16(x)) ? 2 : 0};
     p.db = OpDesc{0, (d->K % 4 == 0 && aligned16(dy)) ? 2 : 0};
     p.C = dw;
-    p.ldc = p.N;
+    p.ldc = No;
     p.accumulate = 0;
     return run(eb, p, a, b, st, static_cast<float *>(workspace));
 }

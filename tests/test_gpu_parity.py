@@ -696,3 +696,28 @@ def test_transposed_orientation_equals_normal(am, luts, orc, model):
     res = orc.gemm(A, B, model, 7)
     assert_tol(outs[0][0], res, "gemm split")
     assert_tol(outs[16][0], res, "gemm split, normal orientation")
+
+
+@pytest.mark.parametrize("force", ["14", "12", "15"])
+def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
+    """Every pass in the transposed orientation (AMSIM_FORCE_CFG >= 10 forces
+    it wherever it is allowed), cp.async operand gathers (C % BN != 0) and TMA
+    alike, against the oracle's sequential order."""
+    lut = luts("mbm")
+    monkeypatch.setenv("AMSIM_FORCE_CFG", force)
+    for k, shape in enumerate([(2, 20, 20, 16, 16, 3, 3, 1, 1), (1, 18, 18, 32, 24, 1, 1, 1, 0),
+                               (2, 16, 16, 64, 32, 3, 3, 1, 1)]):
+        x, w, dy, OH, OW = _conv_tensors(shape, 140 + k)
+        d = am.conv_desc(*shape)
+        od = orc.conv_desc(*shape)
+        with exact_order(am):
+            assert_bits(_run_conv(am, lut, d, x, w, dy, "fwd"), orc.conv_fwd(od, x, w, "mbm").c32, f"{shape} fwd")
+            assert_bits(_run_conv(am, lut, d, x, w, dy, "wgrad"), orc.conv_bwd_filter(od, x, dy, "mbm").c32,
+                        f"{shape} wgrad")
+            assert_bits(_run_conv(am, lut, d, x, w, dy, "dgrad"), orc.conv_bwd_data(od, dy, w, "mbm").c32,
+                        f"{shape} dgrad")
+        assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), orc.conv_bwd_filter(od, x, dy, "mbm"), f"{shape} wgrad split")
+    A = inp.normal((700, 90), 150)
+    B = inp.normal((90, 30), 151)
+    with exact_order(am):
+        assert_bits(run_gemm(am, lut, A, B), orc.gemm(A, B, "mbm", 7).c32, "gemm")
