@@ -217,8 +217,8 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
  *            that are boxes of a tensor -- GEMM operands, conv weights, wgrad
  *            errors, im2col boxes of activations / errors -- are loaded by TMA);
  *   bit 4 -- never use the transposed kernel orientation (default: for a
- *            symmetric table and N <= 128 << M the planner may make the
- *            output channels the warp-shared rows; same bits).
+ *            symmetric table and N << M the planner may make the output
+ *            channels the warp-shared rows; same bits).
  * Errors: AMSIM_ERR_INVALID_ARG outside [0, 31]. */
 amsim_status amsim_set_path_policy(int policy);
 

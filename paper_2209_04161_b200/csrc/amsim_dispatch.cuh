@@ -321,8 +321,8 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
                 break;
             }
     }
-    const bool trn_ok = smem_table && lut->symmetric && pr.nsub == 1 && eb <= 16 && pr.N <= 128 &&
-                        pr.M[0] >= 4 * pr.N && !(policy & 16);
+    const bool trn_ok = smem_table && lut->symmetric && pr.nsub == 1 && eb <= 16 && pr.M[0] >= 4 * pr.N &&
+                        !(policy & 16);
     if (force >= 10 && trn_ok) cands.clear();
     double best = 1e300;
     KParams bestp = p;
@@ -340,9 +340,11 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
             bestp = q;
         }
     }
-    // Transposed orientation for skinny N (the output channels become the
-    // warp-shared rows, the pixels the lanes): symmetric shared-memory tables,
-    // one sub-problem, N well below M (policy bit 4 disables it).
+    // Transposed orientation (the output channels become the warp-shared rows,
+    // the pixels the lanes): symmetric shared-memory tables, one sub-problem,
+    // N well below M (policy bit 4 disables it).  It wins for skinny N (fewer
+    // operand loads per lookup) and, at equal tile shape, whenever the A
+    // operand is a layer input (sparse lanes, see Problem::a_is_activation).
     if (trn_ok) {
         Problem pt = pr;
         pt.N = pr.M[0];
