@@ -721,3 +721,33 @@ def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
     B = inp.normal((90, 30), 151)
     with exact_order(am):
         assert_bits(run_gemm(am, lut, A, B), orc.gemm(A, B, "mbm", 7).c32, "gemm")
+
+
+@pytest.mark.parametrize("force", [None, "14"])
+def test_gemm_accumulate_and_leading_dims_transposed(am, luts, orc, force, monkeypatch):
+    """C += A B with padded leading dimensions in both orientations (the
+    transposed epilogue's read-modify-write path and its split-K reduction)."""
+    if force:
+        monkeypatch.setenv("AMSIM_FORCE_CFG", force)
+    M, N, K = 900, 24, 700
+    Abig = inp.normal((M, K + 3), 161)
+    Bbig = inp.normal((K, N + 5), 162)
+    C0 = inp.normal((M, N + 7), 163)
+    A = dev(Abig)[:, :K]
+    B = dev(Bbig)[:, :N]
+    lut = luts("mbm")
+    res = orc.gemm(Abig[:, :K], Bbig[:, :N], "mbm", 7)
+    for exact in (True, False):
+        C = dev(C0)
+        if exact:
+            with exact_order(am):
+                am.amsim_gemm(lut, A, B, C[:, :N], accumulate=True)
+        else:
+            am.amsim_gemm(lut, A, B, C[:, :N], accumulate=True)
+        got = host(C)
+        if exact:
+            assert_bits(got[:, :N], (C0[:, :N] + res.c32).astype(np.float32), "C + S exact order")
+        else:
+            err = np.abs(got[:, :N].astype(np.float64) - (C0[:, :N].astype(np.float64) + res.c64))
+            assert np.all(err <= 1e-5 * res.abs64 + np.abs(C0[:, :N]) * 2 ** -23 + FLT_MIN)
+        assert_bits(got[:, N:], C0[:, N:], "columns beyond N untouched")
