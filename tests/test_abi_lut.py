@@ -80,8 +80,10 @@ def test_device_entry_width(built):
     # Mitchell: carry + the m-bit sum of the operand mantissas -> 8-bit entries up to m = 7
     assert am.Lut.build("mitchell", 7).info() == (7, 8)
     assert am.Lut.build("mitchell", 8).info() == (8, 16)
-    # exact at m = 3: (8+k)(8+j)/64 has 6 fraction bits -> 8-bit entries
-    assert am.Lut.build("exact", 3).info() == (3, 8)
+    # Mitchell at m = 6 also fits 8 bits, but a 16-bit row of 64 entries is one
+    # wavefront already and the 16-bit path is faster -> 16
+    assert am.Lut.build("mitchell", 6).info() == (6, 16)
+    assert am.Lut.build("exact", 3).info() == (3, 16)
     assert am.Lut.build("exact", 4).info() == (4, 16)
     assert am.Lut.build("exact", 11).info() == (11, 32)
 
