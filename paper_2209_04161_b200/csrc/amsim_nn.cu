@@ -80,6 +80,71 @@ __global__ void __launch_bounds__(NT) channel_partials(int64_t P, int32_t C, F f
     }
 }
 
+// Same with 4 channels per thread (C % 4 == 0, 16-byte aligned tensors):
+// F(row, c4, a, b) accumulates channels 4*c4 .. 4*c4+3; rows are processed two
+// at a time for memory-level parallelism.
+template <class F>
+__global__ void __launch_bounds__(NT) channel_partials4(int64_t P, int32_t C, F f, double2 *part)
+{
+    __shared__ float4 red[2][NT];
+    const int64_t G = gridDim.x;
+    const int64_t r0 = P * blockIdx.x / G, r1 = P * (blockIdx.x + 1) / G;
+    const int tid = threadIdx.x, C4 = C / 4;
+    auto store = [&](int c4, const float4 &a, const float4 &b) {
+        double2 *o = part + blockIdx.x * int64_t(C) + 4 * c4;
+        o[0] = make_double2(a.x, b.x);
+        o[1] = make_double2(a.y, b.y);
+        o[2] = make_double2(a.z, b.z);
+        o[3] = make_double2(a.w, b.w);
+    };
+    if (C4 >= NT) {
+        for (int c4 = tid; c4 < C4; c4 += NT) {
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, a2 = a, b2 = a;
+            int64_t r = r0;
+            for (; r + 1 < r1; r += 2) {
+                f(r, c4, a, b);
+                f(r + 1, c4, a2, b2);
+            }
+            if (r < r1) f(r, c4, a, b);
+            a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
+            b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
+            store(c4, a, b);
+        }
+        return;
+    }
+    const int rp = NT / C4;
+    const int c4 = tid % C4, rl = tid / C4;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, a2 = a, b2 = a;
+    if (rl < rp) {
+        int64_t r = r0 + rl;
+        for (; r + rp < r1; r += 2 * rp) {
+            f(r, c4, a, b);
+            f(r + rp, c4, a2, b2);
+        }
+        if (r < r1) f(r, c4, a, b);
+    }
+    a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
+    b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
+    red[0][tid] = a;
+    red[1][tid] = b;
+    __syncthreads();
+    if (tid < C4) {
+        double sa[4] = {0, 0, 0, 0}, sb[4] = {0, 0, 0, 0};
+        for (int i = 0; i < rp; i++) {
+            float4 u = red[0][i * C4 + tid], v = red[1][i * C4 + tid];
+            sa[0] += u.x; sa[1] += u.y; sa[2] += u.z; sa[3] += u.w;
+            sb[0] += v.x; sb[1] += v.y; sb[2] += v.z; sb[3] += v.w;
+        }
+        double2 *o = part + blockIdx.x * int64_t(C) + 4 * tid;
+        for (int j = 0; j < 4; j++) o[j] = make_double2(sa[j], sb[j]);
+    }
+}
+
+__device__ __forceinline__ void acc4(float4 &a, float x0, float x1, float x2, float x3)
+{
+    a.x += x0; a.y += x1; a.z += x2; a.w += x3;
+}
+
 // fixed-order sum of the partials of channel c
 __device__ __forceinline__ double2 sum_partials(const double2 *part, int64_t G, int32_t C, int c)
 {
@@ -163,6 +228,17 @@ __global__ void __launch_bounds__(NT) bn_apply(const float *x, int64_t n, int32_
     }
 }
 
+struct StatsF4 {
+    const float *x;
+    int32_t C;
+    __device__ __forceinline__ void operator()(int64_t r, int c4, float4 &a, float4 &b) const
+    {
+        float4 v = *reinterpret_cast<const float4 *>(x + r * C + 4 * c4);
+        acc4(a, v.x, v.y, v.z, v.w);
+        acc4(b, v.x * v.x, v.y * v.y, v.z * v.z, v.w * v.w);
+    }
+};
+
 struct BnBwdF {
     const float *dy, *y, *x, *mean, *invstd;
     int32_t C;
@@ -190,6 +266,33 @@ __global__ void bn_bwd_finalize(const double2 *part, int64_t G, int64_t P, int32
     mdzx[c] = float(s.y / double(P));
 }
 
+__global__ void __launch_bounds__(NT) bn_bwd_apply4(const float *dy, const float *y, const float *x, int64_t n,
+                                                    int32_t C, const float *mean, const float *invstd,
+                                                    const float *k1, const float *mdz, const float *mdzx, int relu,
+                                                    float *dx, float *dres)
+{
+    for (int64_t i = (blockIdx.x * int64_t(NT) + threadIdx.x) * 4; i < n; i += int64_t(gridDim.x) * NT * 4) {
+        const int c = int(i % C);
+        float4 g = *reinterpret_cast<const float4 *>(dy + i);
+        if (relu) {
+            float4 o = *reinterpret_cast<const float4 *>(y + i);
+            g.x = o.x > 0.f ? g.x : 0.f; g.y = o.y > 0.f ? g.y : 0.f;
+            g.z = o.z > 0.f ? g.z : 0.f; g.w = o.w > 0.f ? g.w : 0.f;
+        }
+        float4 v = *reinterpret_cast<const float4 *>(x + i);
+        float4 m = *reinterpret_cast<const float4 *>(mean + c), s = *reinterpret_cast<const float4 *>(invstd + c);
+        float4 k = *reinterpret_cast<const float4 *>(k1 + c), z = *reinterpret_cast<const float4 *>(mdz + c);
+        float4 w = *reinterpret_cast<const float4 *>(mdzx + c);
+        float4 r;
+        r.x = k.x * (g.x - z.x - (v.x - m.x) * s.x * w.x);
+        r.y = k.y * (g.y - z.y - (v.y - m.y) * s.y * w.y);
+        r.z = k.z * (g.z - z.z - (v.z - m.z) * s.z * w.z);
+        r.w = k.w * (g.w - z.w - (v.w - m.w) * s.w * w.w);
+        *reinterpret_cast<float4 *>(dx + i) = r;
+        if (dres) *reinterpret_cast<float4 *>(dres + i) = g;
+    }
+}
+
 __global__ void __launch_bounds__(NT) bn_bwd_apply(const float *dy, const float *y, const float *x, int64_t n,
                                                    int32_t C, const float *mean, const float *invstd,
                                                    const float *k1, const float *mdz, const float *mdzx, int relu,
@@ -215,6 +318,28 @@ __global__ void __launch_bounds__(NT) bias_act_fwd_k(const float *x, int64_t n, 
         y[i] = relu ? fmaxf(o, 0.f) : o;
     }
 }
+
+struct BnBwdF4 {
+    const float *dy, *y, *x, *mean, *invstd;
+    int32_t C;
+    int relu;
+    __device__ __forceinline__ void operator()(int64_t r, int c4, float4 &a, float4 &b) const
+    {
+        const int64_t i = r * C + 4 * c4;
+        float4 g = *reinterpret_cast<const float4 *>(dy + i);
+        float4 v = *reinterpret_cast<const float4 *>(x + i);
+        float4 m = *reinterpret_cast<const float4 *>(mean + 4 * c4);
+        float4 s = *reinterpret_cast<const float4 *>(invstd + 4 * c4);
+        if (relu) {
+            float4 o = *reinterpret_cast<const float4 *>(y + i);
+            g.x = o.x > 0.f ? g.x : 0.f; g.y = o.y > 0.f ? g.y : 0.f;
+            g.z = o.z > 0.f ? g.z : 0.f; g.w = o.w > 0.f ? g.w : 0.f;
+        }
+        acc4(a, g.x, g.y, g.z, g.w);
+        acc4(b, g.x * ((v.x - m.x) * s.x), g.y * ((v.y - m.y) * s.y), g.z * ((v.z - m.z) * s.z),
+             g.w * ((v.w - m.w) * s.w));
+    }
+};
 
 struct BiasBwdF {  // writes dx while reducing (each element is visited exactly once)
     const float *dy, *y;
@@ -378,7 +503,14 @@ __global__ void mean_k(const float *v, int N, float *out)
 
 __global__ void __launch_bounds__(NT) add_k(const float *a, const float *b, float *o, int64_t n)
 {
-    for (int64_t i = blockIdx.x * int64_t(NT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * NT) o[i] = a[i] + b[i];
+    const int64_t n4 = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(o)) & 15)
+                           ? 0 : n / 4;
+    for (int64_t i = blockIdx.x * int64_t(NT) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * NT) {
+        float4 u = reinterpret_cast<const float4 *>(a)[i], v = reinterpret_cast<const float4 *>(b)[i];
+        reinterpret_cast<float4 *>(o)[i] = make_float4(u.x + v.x, u.y + v.y, u.z + v.z, u.w + v.w);
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * int64_t(NT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * NT)
+        o[i] = a[i] + b[i];
 }
 
 __global__ void __launch_bounds__(NT) sgd_k(float *w, const float *g, float *v, int64_t n, float lr, float mom,
@@ -433,7 +565,10 @@ amsim_status amsim_bn_fwd_train(const float *x, int64_t P, int32_t C, const floa
     double2 *part = static_cast<double2 *>(ws);
     float *scale = reinterpret_cast<float *>(static_cast<char *>(ws) + G * C * 16);
     float *shift = scale + C;
-    channel_partials<<<int(G), NT, 0, st>>>(P, C, StatsF{x, C}, part);
+    if (C % 4 == 0 && al16(x))
+        channel_partials4<<<int(G), NT, 0, st>>>(P, C, StatsF4{x, C}, part);
+    else
+        channel_partials<<<int(G), NT, 0, st>>>(P, C, StatsF{x, C}, part);
     bn_stats_finalize<<<(C + 127) / 128, 128, 0, st>>>(part, G, P, C, gamma, beta, eps, save_mean, save_invstd,
                                                        running_mean, running_var, momentum, scale, shift);
     const int64_t n = P * C;
@@ -488,10 +623,19 @@ amsim_status amsim_bn_bwd(const float *dy, const float *y, const float *x, int64
     double2 *part = static_cast<double2 *>(ws);
     float *k1 = reinterpret_cast<float *>(static_cast<char *>(ws) + G * C * 16);
     float *mdz = k1 + C, *mdzx = mdz + C;
-    channel_partials<<<int(G), NT, 0, st>>>(P, C, BnBwdF{dy, y, x, save_mean, save_invstd, C, relu}, part);
+    const bool v4 = C % 4 == 0 && al16(dy) && al16(x) && (!y || al16(y)) && al16(dx) && (!dres || al16(dres)) &&
+                    al16(save_mean) && al16(save_invstd);
+    if (v4)
+        channel_partials4<<<int(G), NT, 0, st>>>(P, C, BnBwdF4{dy, y, x, save_mean, save_invstd, C, relu}, part);
+    else
+        channel_partials<<<int(G), NT, 0, st>>>(P, C, BnBwdF{dy, y, x, save_mean, save_invstd, C, relu}, part);
     bn_bwd_finalize<<<(C + 127) / 128, 128, 0, st>>>(part, G, P, C, gamma, save_invstd, dgamma, dbeta, k1, mdz, mdzx);
-    bn_bwd_apply<<<grid_for(P * C), NT, 0, st>>>(dy, y, x, P * C, C, save_mean, save_invstd, k1, mdz, mdzx, relu, dx,
-                                                 dres);
+    if (v4 && al16(k1))
+        bn_bwd_apply4<<<grid_for(P * C / 4), NT, 0, st>>>(dy, y, x, P * C, C, save_mean, save_invstd, k1, mdz, mdzx,
+                                                          relu, dx, dres);
+    else
+        bn_bwd_apply<<<grid_for(P * C), NT, 0, st>>>(dy, y, x, P * C, C, save_mean, save_invstd, k1, mdz, mdzx, relu,
+                                                     dx, dres);
     count_launch(3);
     return check_launch("amsim_bn_bwd");
 }
