@@ -42,7 +42,9 @@ def global_batch(name):
     return {"resnet50": 256, "resnet18": 128, "lenet5": 64}[name]
 
 
-def workload_label(name, model, m):
+def workload_label(name, model, m, size=16384):
+    if name == "gemm":
+        return f"approx GEMM M=N=K={size} (BASELINE.json config 5), {model} LUT m={m}, rows sharded over the GPUs"
     return {"resnet50": "ResNet-50 ImageNet-shaped (224x224x3) train step, global batch 256",
             "resnet18": "ResNet-18 CIFAR-shaped (32x32x3) train step, batch 128",
             "lenet5": "LeNet-5 MNIST-shaped (28x28x1) train step, batch 64"}[name] + f", {model} LUT m={m}"
@@ -104,7 +106,29 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle (as it stands) on a bounded sample of the workload
 
-def oracle_sample(workload: str, model: str, m: int, budget_s: float):
+def oracle_gemm_sample(n: int, model: str, m: int, budget_s: float):
+    """The oracle on whole output rows of the n^3 GEMM (config 5), blocks of
+    max(16, threads) rows (A rows and B drawn from seeded N(0,1) generators, the GPU run's
+    distribution) until `budget_s` is spent."""
+    import numpy as np
+
+    import amsim_inputs as inp
+    import oracle
+    B = inp.normal((n, n), 2)
+    blk = max(16, oracle.num_threads())      # the oracle parallelises over output rows
+    macs, done = 0, 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s and done < n:
+        A = inp.normal((blk, n), 100 + done)
+        oracle.gemm(A, B, model, m)
+        macs += blk * n * n
+        done += blk
+    dt = time.perf_counter() - t0
+    desc = f"{done} output rows of the {n}^3 GEMM ({macs / 1e9:.2f} G approx-MACs), plain-C oracle -O2 OpenMP"
+    return macs, dt, oracle.num_threads(), desc
+
+
+def oracle_sample(workload: str, model: str, m: int, budget_s: float, size: int = 16384):
     """Run the oracle over the workload's layer passes at batch 1 (in step
     order: all forwards, then wgrad/dgrad in reverse) until `budget_s` is
     spent.  Returns (macs, seconds, threads, description)."""
@@ -112,6 +136,8 @@ def oracle_sample(workload: str, model: str, m: int, budget_s: float):
 
     import amsim_inputs as inp
     import oracle
+    if workload == "gemm":
+        return oracle_gemm_sample(size, model, m, budget_s)
     layers, _ = workload_layers(workload, 1)
     passes = [("fwd", l) for l in layers] + [(p, l) for l in layers[::-1] for p in
                                               (("wgrad",) if l.first else ("wgrad", "dgrad"))]
@@ -160,13 +186,13 @@ def run_reference(args):
     import oracle
     oracle.build()
     for _ in range(args.warmup):
-        oracle_sample(args.workload, args.model, args.m, args.ref_budget)
+        oracle_sample(args.workload, args.model, args.m, args.ref_budget, args.size)
     vals, secs = [], []
     macs = 0
     desc = ""
     threads = 0
     for _ in range(args.steps):
-        macs, dt, threads, desc = oracle_sample(args.workload, args.model, args.m, args.ref_budget)
+        macs, dt, threads, desc = oracle_sample(args.workload, args.model, args.m, args.ref_budget, args.size)
         secs.append(dt)
     tot = sum(secs)
     value = macs * args.steps / tot / 1e9
@@ -175,7 +201,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded, shapes and value distributions of the paper's workloads)",
-        "config": {"workload": workload_label(args.workload, args.model, args.m) + " [oracle sample]",
+        "config": {"workload": workload_label(args.workload, args.model, args.m, args.size) + " [oracle sample]",
                    "model": args.model, "m": args.m},
         "cpu_baseline": {"value": value, "unit": "GMAC/s", "cores": threads, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -184,6 +210,143 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# BASELINE.json config 5 at N GPUs: one M = N = K approx GEMM, rows sharded
+
+def run_gemm(args, world, rank, gpu, dev):
+    """rows of A / C partitioned over the ranks, B and the
+    table replicated (B broadcast from rank 0 outside the timed region), no
+    collective on the data path; the all-gather of C is timed separately.
+    value = n^3 approx-MACs / (max over ranks of the device time per GEMM)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from amsim_inputs import device as gen
+    import paper_2209_04161_b200 as am
+    from paper_2209_04161_b200.dp import gather_rows, max_over_ranks, shard_batch, sharded_gemm
+
+    n = args.size
+    lut = am.Lut.build(args.model, args.m)
+    am.amsim_set_path_policy(args.policy)
+    r0, rows = shard_batch(n, world, rank)
+    A = gen.normal((n, n), 1, device=dev)           # every rank reads only its rows
+    B = gen.normal((n, n), 2, device=dev) if rank == 0 else torch.empty((n, n), device=dev)
+    if world > 1:
+        dist.broadcast(B, 0)
+    C = torch.zeros((n, n), device=dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[gpu])
+            else:
+                dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        sharded_gemm(am, lut, A, B, C, world, rank)
+    barrier()
+    # between timed GEMMs: inputs larger than L2 (B is n^2 * 4 B; A's block rows * n * 4 B)
+    clocks = ClockSampler(gpu)
+    clocks.start()
+    launches0 = am.amsim_launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    barrier()
+    for i in range(args.steps):
+        ev[2 * i].record()
+        sharded_gemm(am, lut, A, B, C, world, rank)
+        ev[2 * i + 1].record()
+    barrier()
+    launches = am.amsim_launch_count() - launches0
+    clk = clocks.stop()
+    per = [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps)]
+    ms_local = sum(per) / args.steps
+    ms = max_over_ranks(ms_local, dev)
+    macs = n ** 3
+    value = macs / (ms * 1e-3) / 1e9
+    achieved = rows * n * n / (ms_local * 1e-3) / 1e9     # this rank's kernel rate
+    props = torch.cuda.get_device_properties(dev)
+    sm_max = clk.get("sm_max_mhz") or 1965.0
+    peak = props.multi_processor_count * 32 * sm_max * 1e6 / 1e9
+    lut_meas = None
+    try:
+        idx = np.random.default_rng(0).integers(0, 1 << args.m, 1 << 16).astype(np.uint32)
+        lut_meas = am.amsim_bench_lut_lookup(args.m, lut.info()[1], idx, iters=2048) / 1e9
+    except Exception as ex:  # noqa: BLE001
+        lut_meas = f"unavailable: {ex}"
+
+    gather_ms = None
+    if world > 1:
+        out = torch.empty_like(C)
+        gather_rows(C[r0:r0 + rows], n, world, out)
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(args.steps):
+            gather_rows(C[r0:r0 + rows], n, world, out)
+        g1.record()
+        barrier()
+        gather_ms = max_over_ranks(g0.elapsed_time(g1) / args.steps, dev)
+        del out
+
+    # end to end through the public API: this rank's A rows and B from pinned host
+    # memory, the GEMM, this rank's C rows back to pinned host memory, every step
+    e2e = None
+    if not args.no_e2e:
+        hA = torch.empty((rows, n), pin_memory=True)
+        hA.copy_(A[r0:r0 + rows])
+        hB = torch.empty((n, n), pin_memory=True)
+        hB.copy_(B)
+        hC = torch.empty((rows, n), pin_memory=True)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            A[r0:r0 + rows].copy_(hA, non_blocking=True)
+            B.copy_(hB, non_blocking=True)
+            sharded_gemm(am, lut, A, B, C, world, rank)
+            hC.copy_(C[r0:r0 + rows], non_blocking=True)
+        f1.record()
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1) / args.steps, dev)
+        e2e = {"value": macs / (ems * 1e-3) / 1e9, "unit": "GMAC/s", "h2d_bytes_per_step": 4 * (rows * n + n * n),
+               "d2h_bytes_per_step": 4 * rows * n, "ms_per_step": ems}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cm, dt, threads, desc = oracle_gemm_sample(n, args.model, args.m, args.cpu_budget)
+            cpu = {"value": cm / dt / 1e9, "unit": "GMAC/s", "cores": threads, "kind": "oracle", "sample": desc}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GMAC/s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GMAC/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; A, B ~ N(0,1))",
+            "config": {"workload": workload_label("gemm", args.model, args.m, n), "M": n, "N": n, "K": n,
+                       "model": args.model, "m": args.m, "rows_per_gpu": [shard_batch(n, world, r)[1]
+                                                                          for r in range(world)],
+                       "parallelism": f"M-sharded over {world} GPU(s), B replicated",
+                       "l2": f"inputs larger than L2 (B = {4 * n * n / 1e6:.0f} MB)" if 4 * n * n > 126e6
+                       else "operands fit the 126 MB L2; not flushed"},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "allgather_ms": gather_ms,
+            "roofline": {"bound": "alu", "kernel": "amsim_mm_kernel [gemm]", "achieved": achieved, "peak": peak,
+                         "unit": "GMAC/s", "frac": achieved / peak, "traffic": None,
+                         "algorithmic_bytes_per_launch": 4 * (2 * rows * n + n * n),
+                         "frac_of_measured_lookup": (achieved / lut_meas) if isinstance(lut_meas, float) else None,
+                         "peak_basis": "148 SMs x 32 LUT lookups/clk x max SM clock",
+                         "lut_lookup_measured_gps": lut_meas, "ms_per_launch": per},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -191,7 +354,10 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="amsim", choices=["amsim", "reference"])
-    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "resnet18", "lenet5"])
+    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "resnet18", "lenet5", "gemm"],
+                    help="gemm = BASELINE.json config 5: one M = N = K = --size approx GEMM, rows sharded over "
+                         "the GPUs (strong scaling)")
+    ap.add_argument("--size", type=int, default=16384, help="--workload gemm: M = N = K")
     ap.add_argument("--model", default="mbm", choices=["mbm", "exact", "mitchell"])
     ap.add_argument("--m", type=int, default=7)
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
@@ -235,6 +401,12 @@ def main():
     import paper_2209_04161_b200 as am
     from paper_2209_04161_b200.dp import max_over_ranks, shard_batch
     from paper_2209_04161_b200.train_step import TrainStep
+
+    if args.workload == "gemm":
+        run_gemm(args, world, rank, gpu, dev)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     gb = global_batch(args.workload)
     _, nb = shard_batch(gb, world, rank)

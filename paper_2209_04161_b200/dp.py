@@ -18,6 +18,44 @@ def shard_batch(global_batch: int, world: int, rank: int):
     return start, count
 
 
+def sharded_gemm(am, lut, A, B, C, world: int, rank: int, stream=None):
+    """SURVEY.md §8(e), GEMM (config 5): rows of A and C are partitioned into
+    `world` contiguous blocks (shard_batch); B and the table are replicated.
+    Rank `rank` computes C[r0:r0+n] = A[r0:r0+n] · B through amsim_gemm.  The
+    rows of an AMSim GEMM are independent and the per-row summation order does
+    not depend on M, so the blocks are bit-identical to the same rows of the
+    single-GPU result (tests/test_gpu_parity.py::test_gemm_row_shards_bit_identical).
+    A [M, K] and C [M, N] are the full row-major matrices (only this rank's
+    rows of A are read and of C written).  Returns (r0, n)."""
+    if C.shape[0] != A.shape[0]:
+        raise ValueError("A and C must have the same number of rows")
+    r0, n = shard_batch(C.shape[0], world, rank)
+    if n:
+        am.amsim_gemm(lut, A[r0:r0 + n], B, C[r0:r0 + n], stream=stream)
+    return r0, n
+
+
+def gather_rows(C_local, M: int, world: int, out=None):
+    """All-gather the row blocks of sharded_gemm into the full M-row matrix on
+    every rank (NCCL all_gather_into_tensor on equal, padded blocks; the
+    optional, separately timed step of §8(e)).  C_local holds this rank's
+    shard_batch rows.  Returns the gathered [M, N] tensor."""
+    import torch
+    import torch.distributed as dist
+    rows = -(-M // world)
+    N = C_local.shape[1]
+    pad = torch.zeros((rows, N), dtype=C_local.dtype, device=C_local.device)
+    pad[:C_local.shape[0]].copy_(C_local)
+    full = torch.empty((rows * world, N), dtype=C_local.dtype, device=C_local.device)
+    dist.all_gather_into_tensor(full, pad)
+    if out is None:
+        out = torch.empty((M, N), dtype=C_local.dtype, device=C_local.device)
+    for r in range(world):
+        s, n = shard_batch(M, world, r)
+        out[s:s + n].copy_(full[r * rows:r * rows + n])
+    return out
+
+
 @dataclass
 class Bucket:
     layers: list            # layer indices (in the order their gradients become ready)

@@ -111,3 +111,56 @@ def test_single_process_reducer_is_noop():
     red.ready(0)
     red.finish()
     assert torch.equal(flat, torch.arange(total, dtype=torch.float32))
+
+
+class _OracleGemm:
+    """Stand-in for the binding's amsim_gemm on CPU tensors (test-only): the
+    oracle's FP32 c32 result of the same rows."""
+
+    @staticmethod
+    def amsim_gemm(lut, A, B, C, stream=None):
+        import oracle
+        C.copy_(torch.from_numpy(oracle.gemm(A.numpy(), B.numpy(), "mitchell", 7).c32))
+        return C
+
+
+def _gemm_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import amsim_inputs as inp
+        import oracle
+        from paper_2209_04161_b200.dp import gather_rows, sharded_gemm
+        M, N, K = 7, 5, 9          # ragged: 4 + 3 rows
+        A = torch.from_numpy(inp.normal((M, K), 1))
+        B = torch.from_numpy(inp.normal((K, N), 2))
+        C = torch.full((M, N), float("nan"))
+        r0, n = sharded_gemm(_OracleGemm, None, A, B, C, world, rank)
+        untouched = bool(torch.isnan(torch.cat([C[:r0], C[r0 + n:]])).all())
+        full = gather_rows(C[r0:r0 + n], M, world)
+        ref = oracle.gemm(A.numpy(), B.numpy(), "mitchell", 7).c32
+        same = np.array_equal(full.numpy().view(np.uint32), ref.view(np.uint32))
+        q.put((rank, r0, n, untouched, same))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_gemm_rows_and_gather():
+    """SURVEY.md §8(e) GEMM: M rows partitioned over 2 ranks, each writes only
+    its rows, the all-gather reassembles the single-process result bit-exactly."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gemm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [(r0, n) for _, r0, n, _, _ in res] == [(0, 4), (4, 3)]
+    for rank, _, _, untouched, same in res:
+        assert untouched, f"rank {rank} wrote rows outside its shard"
+        assert same, f"rank {rank}: gathered rows differ from the single-process GEMM"

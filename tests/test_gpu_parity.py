@@ -751,3 +751,61 @@ def test_gemm_accumulate_and_leading_dims_transposed(am, luts, orc, force, monke
             err = np.abs(got[:, :N].astype(np.float64) - (C0[:, :N].astype(np.float64) + res.c64))
             assert np.all(err <= 1e-5 * res.abs64 + np.abs(C0[:, :N]) * 2 ** -23 + FLT_MIN)
         assert_bits(got[:, N:], C0[:, N:], "columns beyond N untouched")
+
+
+# ---------------------------------------------------------------------------
+# M-sharded GEMM (SURVEY.md §8(e), config 5 at N GPUs)
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_gemm_row_shards_bit_identical(am, luts, orc, world):
+    """Each rank's row block (dp.sharded_gemm: amsim_gemm on A[r0:r0+n], C[r0:r0+n])
+    in exact order is bit-identical to the single-GPU GEMM and the oracle's c32;
+    in the default launch configuration (the planner may pick other tiles /
+    split-K for the smaller M) it meets the GEMM tolerance against the oracle."""
+    import torch
+    from paper_2209_04161_b200.dp import sharded_gemm
+    M, N, K = 1000, 384, 1040
+    Ah, Bh = inp.normal((M, K), 41), inp.normal((K, N), 42)
+    A, B = dev(Ah), dev(Bh)
+    res = orc.gemm(Ah, Bh, "mitchell", 7)
+    lut = luts("mitchell")
+    for policy in (0, 2):
+        am.amsim_set_path_policy(policy)
+        try:
+            C = torch.full((M, N), float("nan"), device="cuda")
+            cover = np.zeros(M, int)
+            for r in range(world):
+                r0, n = sharded_gemm(am, lut, A, B, C, world, r)
+                cover[r0:r0 + n] += 1
+            assert (cover == 1).all()
+            if policy == 2:
+                full = torch.empty((M, N), device="cuda")
+                am.amsim_gemm(lut, A, B, full)
+                assert_bits(host(C), host(full), f"world {world}: shards vs one GEMM")
+                assert_bits(host(C), res.c32, f"world {world}: shards vs oracle c32")
+            else:
+                assert_tol(host(C), res, f"world {world}")
+        finally:
+            am.amsim_set_path_policy(0)
+
+
+def test_gemm_16384_rank_block_sampled(am, luts, orc):
+    """Config 5 at full size in the bench's launch configuration
+    (bench.py --workload gemm): the last rank's block of 16384^3 at 8 GPUs
+    (2048 x 16384 x 16384, Mitchell m = 7), sampled rows against the oracle."""
+    import torch
+    from amsim_inputs import device as gen
+    from paper_2209_04161_b200.dp import sharded_gemm
+    n = 16384
+    A = gen.normal((n, n), 1, device="cuda")
+    B = gen.normal((n, n), 2, device="cuda")
+    C = torch.full((n, n), float("nan"), device="cuda")
+    r0, rows = sharded_gemm(am, luts("mitchell"), A, B, C, 8, 7)
+    assert (r0, rows) == (14336, 2048)
+    sample = np.array([r0, r0 + 1, r0 + 977, n - 1])
+    Ah = A[torch.from_numpy(sample).cuda()].cpu().numpy()
+    res = orc.gemm(Ah, B.cpu().numpy(), "mitchell", 7)
+    assert_tol(host(C)[sample], res, "16384^3 rank 7 of 8")
+    assert torch.isnan(C[:r0]).all()
+    del A, B, C
+    torch.cuda.empty_cache()
