@@ -285,8 +285,10 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     p.policy = policy & 1;
     const bool smem_table = !p.lut_global && p.mul == MUL_LUT;
     const uint32_t smem_lut = smem_table ? bytes : 0u;
+    int force = -1;   // AMSIM_FORCE_CFG: tuning experiments only (>= 10: transposed orientation, cfg - 10)
+    if (const char *f = std::getenv("AMSIM_FORCE_CFG"); f && *f) force = std::atoi(f);
     std::vector<int64_t> key = {pr.N, pr.nsub, pr.max_splits, pr.a_is_activation, eb, p.lut_global, p.mul, policy & (3 | 16), mbits,
-                                num_sms()};
+                                num_sms(), force};
     for (int i = 0; i < pr.nsub; i++) {
         key.push_back(pr.M[i]);
         key.push_back(pr.K[i]);
@@ -312,9 +314,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     } else {
         cands = {CfgId::Big, CfgId::Lean};
     }
-    int force = -1;   // AMSIM_FORCE_CFG: tuning experiments only (>= 10: transposed orientation, cfg - 10)
-    if (const char *f = std::getenv("AMSIM_FORCE_CFG")) {
-        force = std::atoi(f);
+    if (force >= 0) {
         for (CfgId c : cands)
             if (int(c) == force) {
                 cands = {c};
