@@ -322,7 +322,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
             }
     }
     const bool trn_ok = smem_table && lut->symmetric && pr.nsub == 1 && eb <= 16 &&
-                        int64_t(pr.M[0]) * 4 >= pr.N && !(policy & 16);
+                        int64_t(pr.M[0]) * 4 >= pr.N && !(policy & 16) && !(force >= 0 && force < 10);
     if (force >= 10 && trn_ok) cands.clear();
     double best = 1e300;
     KParams bestp = p;
