@@ -110,8 +110,6 @@ def oracle_gemm_sample(n: int, model: str, m: int, budget_s: float):
     """The oracle on whole output rows of the n^3 GEMM (config 5), blocks of
     max(16, threads) rows (A rows and B drawn from seeded N(0,1) generators, the GPU run's
     distribution) until `budget_s` is spent."""
-    import numpy as np
-
     import amsim_inputs as inp
     import oracle
     B = inp.normal((n, n), 2)

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--m", type=int, default=7)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--top", type=int, default=25)
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the workload's global batch)")
     args = ap.parse_args()
 
     import torch
@@ -32,7 +33,7 @@ def main():
     import paper_2209_04161_b200 as am
     from paper_2209_04161_b200.train_step import TrainStep
 
-    batch = {"resnet50": 256, "resnet18": 128, "lenet5": 64}[args.workload]
+    batch = args.batch or {"resnet50": 256, "resnet18": 128, "lenet5": 64}[args.workload]
     layers = {"resnet50": inp.resnet50_layers, "resnet18": inp.resnet18_cifar_layers,
               "lenet5": inp.lenet5_layers}[args.workload](batch)
     lut = am.Lut.build(args.model, args.m)
@@ -68,7 +69,7 @@ def main():
     for r in rows:
         r["lost_ms"] = r["ms"] - r["ms"] * r["tmacs"] / best
     rows.sort(key=lambda r: -r["lost_ms"])
-    print(json.dumps({"total_ms": total, "best_tmacs": best, "lost_ms": sum(r["lost_ms"] for r in rows)}))
+    print(json.dumps({"batch": batch, "total_ms": total, "tmacs": sum(l.macs() for _, _, l in names) / (total * 1e-3) / 1e12, "best_tmacs": best, "lost_ms": sum(r["lost_ms"] for r in rows)}))
     for r in rows[:args.top]:
         print(json.dumps(r))
 
