@@ -449,14 +449,22 @@ struct DgW {
 
 // ---------------------------------------------------------------------------
 
-template <int NT_, int TM_, int TN_>
+// NT threads as WM x WN warps (WN = warps side by side along N); each warp owns
+// TM rows x 32*TN columns of the BM x BN CTA tile.
+template <int NT_, int TM_, int TN_, int WN_ = 1>
 struct KCfg {
     static constexpr int NT = NT_;
     static constexpr int NWARPS = NT / 32;
     static constexpr int TM = TM_;
     static constexpr int TN = TN_;
-    static constexpr int BM = NWARPS * TM;
-    static constexpr int BN = 32 * TN;
+    static constexpr int WN = WN_;
+    static constexpr int WM = NWARPS / WN;
+    static_assert(WM * WN == NWARPS, "warp grid must cover the CTA");
+    static constexpr int BM = WM * TM;
+    static constexpr int BN = WN * 32 * TN;
+    // first row / column of warp w's sub-tile
+    static constexpr __host__ __device__ int wrow(int w) { return (w / WN) * TM; }
+    static constexpr __host__ __device__ int wcol(int w) { return (w % WN) * 32 * TN; }
     // a lane owns columns lane * CG + col(c), c < TN: groups of 4 consecutive
     // columns 128 apart when TN >= 4 (conflict-free LDS.128), else TN consecutive
     static constexpr int CG = TN >= 4 ? 4 : TN;
@@ -769,10 +777,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             const bool fast = p.policy == 0 && Amax <= 254 && Bmax <= 253 &&
                               (Amax == 0 || Bmax == 0 || (Amin + Bmin >= 128 && Amax + Bmax <= 380));
 
-            const uint32_t *A_al = a_al + warp * TM, *A_off = a_off + warp * TM;
+            const uint32_t *A_al = a_al + Cf::wrow(warp), *A_off = a_off + Cf::wrow(warp);
             // lane columns: groups of 4 consecutive columns, group g at g * 128
             // (TN >= 4: each LDS.128 of a group covers 512 contiguous bytes), else TN consecutive
-            const uint32_t *B_al = b_al + lane * CG, *B_off = b_off + lane * CG;
+            const uint32_t *B_al = b_al + Cf::wcol(warp) + lane * CG, *B_off = b_off + Cf::wcol(warp) + lane * CG;
             if constexpr (MUL == MUL_NATIVE) {
                 // native FP32 multiply-add of the untruncated operands (IEEE, no FTZ)
 #pragma unroll 2
@@ -896,10 +904,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
         float *Cb = split_out ? p.ws + S.ws_offset + int64_t(T.split) * S.M * p.N : p.C;
         if constexpr (TRN) {
             if (!split_out) {
-                const int row0 = T.m0 + warp * TM;
+                const int row0 = T.m0 + Cf::wrow(warp);
 #pragma unroll
                 for (int c = 0; c < TN; c++) {
-                    int col = T.n0 + lane * CG + Cf::col(c);
+                    int col = T.n0 + Cf::wcol(warp) + lane * CG + Cf::col(c);
                     if (col >= p.N) continue;
                     float *dst = p.C + opb.out_row(T.s, col, p.ldc) + row0;
                     if (row0 + TM <= S.M && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && !p.accumulate) {
@@ -918,7 +926,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
         }
 #pragma unroll
         for (int r = 0; r < TM; r++) {
-            int row = T.m0 + warp * TM + r;
+            int row = T.m0 + Cf::wrow(warp) + r;
             if (row >= S.M) continue;
             int64_t off;
             if constexpr (TRN)
@@ -928,7 +936,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             float *dst = Cb + off;
 #pragma unroll
             for (int c = 0; c < TN; c++) {
-                int col = T.n0 + lane * CG + Cf::col(c);
+                int col = T.n0 + Cf::wcol(warp) + lane * CG + Cf::col(c);
                 if (col >= p.N) continue;
                 dst[col] = (p.accumulate && !split_out) ? (dst[col] + acc[r][c]) : acc[r][c];
             }

@@ -94,6 +94,8 @@ using CfgBig = KCfg<AMSIM_NT_BIG, AMSIM_TM_BIG, AMSIM_TN_BIG>;  // N > 64, M > 6
 using CfgLean = KCfg<256, 8, 2>;                         // N <= 64, M <= 64; and tables too large for the others
 using CfgWide = KCfg<256, 8, 4>;                         // N > 64, M <= 64
 using CfgHuge = KCfg<256, 16, 8>;                        // N >= 256, 16/32-bit tables (fewer operand loads per lookup)
+using CfgFlat = KCfg<256, 16, 4, 2>;                     // 64 x 256: 64-row problems (64-channel layers, transposed)
+                                                         // with Big's 16 x 4 register tile instead of Wide's 8 x 4
 
 static int g_num_sms = 0;
 static int num_sms()
@@ -127,7 +129,7 @@ struct Problem {
     bool a_is_activation = false;
 };
 
-enum class CfgId { Small, Mid, Big, Lean, Wide, Huge };
+enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat };
 static constexpr size_t kSmemMax = 227 * 1024;
 
 static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t lut_bytes)
@@ -138,6 +140,7 @@ static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t
     case CfgId::Lean: BM = CfgLean::BM; BN = CfgLean::BN; NT = CfgLean::NT; smem = CfgLean::smem_bytes(lut_bytes); break;
     case CfgId::Wide: BM = CfgWide::BM; BN = CfgWide::BN; NT = CfgWide::NT; smem = CfgWide::smem_bytes(lut_bytes); break;
     case CfgId::Huge: BM = CfgHuge::BM; BN = CfgHuge::BN; NT = CfgHuge::NT; smem = CfgHuge::smem_bytes(lut_bytes); break;
+    case CfgId::Flat: BM = CfgFlat::BM; BN = CfgFlat::BN; NT = CfgFlat::NT; smem = CfgFlat::smem_bytes(lut_bytes); break;
     default: BM = CfgBig::BM; BN = CfgBig::BN; NT = CfgBig::NT; smem = CfgBig::smem_bytes(lut_bytes); break;
     }
 }
@@ -232,6 +235,7 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
     case CfgId::Lean: TM = 8; TN = 2; break;
     case CfgId::Wide: TM = 8; TN = 4; break;
     case CfgId::Huge: TM = 16; TN = 8; break;
+    case CfgId::Flat: TM = 16; TN = 4; break;
     default: break;
     }
     double row = double(size_t(1) << mbits) * (eb / 8);
@@ -309,7 +313,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     // only); cost = planned makespan in k-tiles x lookups per k-tile x wavefronts per lookup.
     std::vector<CfgId> cands;
     if (smem_table) {
-        cands = {CfgId::Small, CfgId::Mid, CfgId::Big, CfgId::Lean, CfgId::Wide};
+        cands = {CfgId::Small, CfgId::Mid, CfgId::Big, CfgId::Lean, CfgId::Wide, CfgId::Flat};
         if (eb >= 16) cands.push_back(CfgId::Huge);
     } else {
         cands = {CfgId::Big, CfgId::Lean};
@@ -349,7 +353,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         Problem pt = pr;
         pt.N = pr.M[0];
         pt.M[0] = pr.N;
-        std::vector<CfgId> tc = {CfgId::Wide, CfgId::Big};
+        std::vector<CfgId> tc = {CfgId::Wide, CfgId::Big, CfgId::Flat};
         if (eb >= 16) tc.push_back(CfgId::Huge);
         if (force >= 10) tc = {CfgId(force - 10)};
         if (force >= 10 && CfgId(force - 10) == CfgId::Huge && eb < 16) tc = {CfgId::Big};
@@ -432,6 +436,7 @@ static amsim_status launch_eb(const KParams &p, const OpA &a, const OpB &b, cuda
     case CfgId::Mid: return launch_cfg<CfgMid, EB>(p, a, b, st);
     case CfgId::Lean: return launch_cfg<CfgLean, EB>(p, a, b, st);
     case CfgId::Wide: return launch_cfg<CfgWide, EB>(p, a, b, st);
+    case CfgId::Flat: return launch_cfg<CfgFlat, EB>(p, a, b, st);
     case CfgId::Huge:
         if constexpr (EB >= 16) return launch_cfg<CfgHuge, EB>(p, a, b, st);
         else return set_error(AMSIM_ERR_UNSUPPORTED, "internal: Huge tiles need 16/32-bit tables");
@@ -614,6 +619,7 @@ static amsim_status launch_trn(const KParams &p, const OpR &r, const OpC &c, cud
 {
     switch (CfgId(p.cfg)) {
     case CfgId::Wide: return launch_cfg<CfgWide, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
+    case CfgId::Flat: return launch_cfg<CfgFlat, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Big: return launch_cfg<CfgBig, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Huge:
         if constexpr (EB >= 16) return launch_cfg<CfgHuge, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);

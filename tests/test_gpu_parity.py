@@ -698,7 +698,7 @@ def test_transposed_orientation_equals_normal(am, luts, orc, model):
     assert_tol(outs[16][0], res, "gemm split, normal orientation")
 
 
-@pytest.mark.parametrize("force", ["14", "12", "15"])
+@pytest.mark.parametrize("force", ["14", "12", "15", "16", "6"])
 def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
     """Every pass in the transposed orientation (AMSIM_FORCE_CFG >= 10 forces
     it wherever it is allowed), cp.async operand gathers (C % BN != 0) and TMA
@@ -723,7 +723,7 @@ def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
         assert_bits(run_gemm(am, lut, A, B), orc.gemm(A, B, "mbm", 7).c32, "gemm")
 
 
-@pytest.mark.parametrize("force", [None, "14"])
+@pytest.mark.parametrize("force", [None, "14", "16", "6"])
 def test_gemm_accumulate_and_leading_dims_transposed(am, luts, orc, force, monkeypatch):
     """C += A B with padded leading dimensions in both orientations (the
     transposed epilogue's read-modify-write path and its split-K reduction)."""
