@@ -8,3 +8,6 @@ timeout 900 python tools/paper_ratios.py > gpurun_out/ratios.jsonl 2> gpurun_out
 timeout 1200 python tools/full_step.py > gpurun_out/full_step.jsonl 2> gpurun_out/full_step.err
 timeout 300 python bench.py --model mitchell --no-cpu-baseline > gpurun_out/bench_mitchell.jsonl 2> gpurun_out/bench_mitchell.err
 for f in gpurun_out/*.err; do tail -n 2 $f; done
+timeout 300 python bench.py --workload gemm --model mitchell > gpurun_out/bench_gemm.jsonl 2> gpurun_out/bench_gemm.err
+timeout 300 python tools/layer_table.py --top 40 > gpurun_out/layer_table.jsonl 2> gpurun_out/layer_table.err
+for B in 32 64 128 256; do timeout 300 python tools/layer_table.py --batch $B --top 0 | head -1; done > gpurun_out/batch_scaling.jsonl 2> gpurun_out/batch_scaling.err
