@@ -220,8 +220,11 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
  *            errors, im2col boxes of activations / errors -- are loaded by TMA);
  *   bit 4 -- never use the transposed kernel orientation (default: for a
  *            symmetric table and N << M the planner may make the output
- *            channels the warp-shared rows; same bits).
- * Errors: AMSIM_ERR_INVALID_ARG outside [0, 31]. */
+ *            channels the warp-shared rows; same bits);
+ *   bit 5 -- gather wgrad activation tiles that span several taps with
+ *            cp.async (default: when the tile's rows are a multiple of a
+ *            power-of-two C >= 32, one TMA im2col box per tap).
+ * Errors: AMSIM_ERR_INVALID_ARG outside [0, 63]. */
 amsim_status amsim_set_path_policy(int policy);
 
 /* Multiply mode (process-wide, default AMSIM_MUL_LUT).  The two other modes

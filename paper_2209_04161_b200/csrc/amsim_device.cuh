@@ -205,8 +205,10 @@ struct SubP {
 
 struct OpDesc {
     int kcontig;          // raw tile stored [mn][BK + RAW_PAD] (k contiguous, 1), [BK][BMN] (0), or
-                          // [mn][BK] with TMA's 64-byte swizzle (k contiguous, TMA-loaded, 2)
+                          // [mn][BK] with TMA's 64-byte swizzle (k contiguous, TMA-loaded, 2), or
+                          // tap-blocked [BMN / 2^cblk_log2][BK][2^cblk_log2] (one im2col box per tap, 3)
     int vec_log2;         // 0 (4-byte copies) or 2 (16-byte copies along the contiguous dim)
+    int cblk_log2;        // kcontig 3: channels per tap block (log2)
 };
 
 struct KParams {
@@ -329,7 +331,9 @@ struct WgX {
     // TMA box origin.  1x1 / stride 1 / unpadded: element (ci, pixel) of x as
     // [pixels][C] (2-D).  Otherwise im2col mode (C % BM == 0, so a row tile lies
     // in one tap): BK output pixels from the k-tile's first (n, oh, ow), BM
-    // channels from the row tile's (kh, kw, ci0) -- smem [BK][BM].
+    // channels from the row tile's (kh, kw, ci0) -- smem [BK][BM].  When BM is a
+    // multiple of C instead (multi-tap, kcontig 3), one box of C channels per tap
+    // of the row tile, called with mn0 = the tap block's first row.
     __device__ __forceinline__ void tma_coords(int, int mn0, int k0, int *c) const
     {
         if (g.R == 1 && g.S == 1 && g.sh == 1 && g.sw == 1 && g.ph == 0 && g.pw == 0) {
@@ -342,6 +346,10 @@ struct WgX {
         uint32_t kw = g.fC.div(r2), ci = r2 - kw * g.C;
         uint32_t n = g.fOHOW.div(uint32_t(k0)), r = uint32_t(k0) - n * uint32_t(g.OH * g.OW);
         uint32_t oh = g.fOW.div(r), ow = r - oh * g.OW;
+        if (mn0 >= M) {   // tap block past the last tap (multi-tap boxes): channels out of range, zero-filled
+            kh = kw = 0;
+            ci = uint32_t(g.C);
+        }
         c[0] = int(ci);
         c[1] = int(ow) * g.sw - g.pw;
         c[2] = int(oh) * g.sh - g.ph;
@@ -523,9 +531,9 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
 // PACK: one word per element, alpha (bits 31..23) | offset (bits 22..0; shared
 // memory table offsets are < 2^18), halving the inner loop's operand loads.
 template <int NT, int ROWS, bool RAW_ALPHA = false, bool PACK = false>
-__device__ __forceinline__ void decode_operand(const float *raw, int kcontig, uint32_t *al, uint32_t *off, int shift,
-                                               uint32_t mask, int off_shift, uint32_t off_base, uint32_t &emin,
-                                               uint32_t &emax, uint32_t elo, uint32_t ehi)
+__device__ __forceinline__ void decode_operand(const float *raw, int kcontig, int cbl, uint32_t *al, uint32_t *off,
+                                               int shift, uint32_t mask, int off_shift, uint32_t off_base,
+                                               uint32_t &emin, uint32_t &emax, uint32_t elo, uint32_t ehi)
 {
     constexpr int total = BK * ROWS;
 #pragma unroll
@@ -537,6 +545,8 @@ __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, ui
             if (kcontig == 2) {  // TMA tile [ROWS][BK] with the 64-byte swizzle: 16-B chunk ^= address bits 8..7
                 uint32_t a = smem_u32(raw) + uint32_t(i * BK + kk) * 4u;
                 v = lds_f32(a ^ (((a >> 7) & 3u) << 4));
+            } else if (kcontig == 3) {  // tap-blocked [ROWS >> cbl][BK][1 << cbl]
+                v = raw[(((i >> cbl) * BK + kk) << cbl) | (i & ((1 << cbl) - 1))];
             } else {
                 v = kcontig ? raw[i * (BK + RAW_PAD) + kk] : raw[kk * ROWS + i];
             }
@@ -706,14 +716,21 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                         else if (mode == 3) tma_load_3d(dst, map, c[0], c[1], c[2], bar);
                         else tma_load_2d(dst, map, c[0], c[1], bar);
                     };
-                    if (p.tma_on[0]) {
-                        opa.tma_coords(IT.s, IT.m0, k0, c);
-                        load(p.tma_on[0], &p.tma[0], smem_u32(ra));
-                    }
-                    if (p.tma_on[1]) {
-                        opb.tma_coords(IT.s, IT.n0, k0, c);
-                        load(p.tma_on[1], &p.tma[1], smem_u32(rb));
-                    }
+                    // mode 5: one im2col box of 2^cblk_log2 channels per tap block of the tile
+                    auto load_op = [&](int mode, const CUtensorMap *map, uint32_t dst, const auto &op, int mn0,
+                                       int rows, int cbl) {
+                        if (mode == 5) {
+                            for (int t = 0; t < (rows >> cbl); t++) {
+                                op.tma_coords(IT.s, mn0 + (t << cbl), k0, c);
+                                load(4, map, dst + uint32_t(t * (BK << cbl)) * 4u);
+                            }
+                        } else {
+                            op.tma_coords(IT.s, mn0, k0, c);
+                            load(mode, map, dst);
+                        }
+                    };
+                    if (p.tma_on[0]) load_op(p.tma_on[0], &p.tma[0], smem_u32(ra), opa, IT.m0, BM, p.da.cblk_log2);
+                    if (p.tma_on[1]) load_op(p.tma_on[1], &p.tma[1], smem_u32(rb), opb, IT.n0, BN, p.db.cblk_log2);
                 }
             }
             if (!p.tma_on[0]) issue_operand<NT, BM>(opa, p.da, ra, IT.s, IT.m0, k0, IT.ke, dummy);
@@ -749,9 +766,9 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             uint32_t *d = dec + (g & 1) * Cf::DEC;
             uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + 2 * BK * BM, *b_off = b_al + BK * BN;
             uint32_t amin = 255, amax = 0, bmin = 255, bmax = 0;
-            decode_operand<NT, BM, MUL == MUL_NATIVE, PK>(ra, p.da.kcontig, a_al, a_off, shift, mask, a_off_shift,
+            decode_operand<NT, BM, MUL == MUL_NATIVE, PK>(ra, p.da.kcontig, p.da.cblk_log2, a_al, a_off, shift, mask, a_off_shift,
                                                           a_off_base, amin, amax, elo, ehi);
-            decode_operand<NT, BN, MUL == MUL_NATIVE, PK>(rb, p.db.kcontig, b_al, b_off, shift, mask, b_off_shift,
+            decode_operand<NT, BN, MUL == MUL_NATIVE, PK>(rb, p.db.kcontig, p.db.cblk_log2, b_al, b_off, shift, mask, b_off_shift,
                                                           b_off_base, bmin, bmax, elo, ehi);
             amin = __reduce_min_sync(0xffffffffu, amin);
             amax = __reduce_max_sync(0xffffffffu, amax);

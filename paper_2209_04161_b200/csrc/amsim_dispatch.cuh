@@ -562,14 +562,25 @@ static int setup_tma(CUtensorMap *map, const FwdX &op, int rows, OpDesc &d)
 
 // conv wgrad A: for 1x1 / stride 1 / unpadded, element (ci, pixel) of x as [pixels][C];
 // otherwise im2col mode with BK pixels x `rows` channels per box when C % rows == 0
-static int setup_tma(CUtensorMap *map, const WgX &op, int rows, OpDesc &)
+static int setup_tma(CUtensorMap *map, const WgX &op, int rows, OpDesc &d)
 {
     if (tma_disabled()) return 0;
     if (!is_1x1_s1(op.g)) {
         const ConvGeom &g = op.g;
         if (rows > 256) return 0;
-        return encode_im2col(map, op.x, g.N, g.H, g.W, g.C, -g.ph, -g.pw, g.ph - (g.R - 1), g.pw - (g.S - 1), g.sh,
-                             g.sw, BK, rows);
+        if (g.C % rows == 0)
+            return encode_im2col(map, op.x, g.N, g.H, g.W, g.C, -g.ph, -g.pw, g.ph - (g.R - 1), g.pw - (g.S - 1),
+                                 g.sh, g.sw, BK, rows);
+        // multi-tap: a row tile spans rows / C whole taps (C a power of two, >= 32 so
+        // the plain [BK][C] box needs no swizzle): one im2col box per tap, smem
+        // tap-blocked [rows / C][BK][C] (kcontig 3, tap-block loop in the kernel)
+        if (rows % g.C || (g.C & (g.C - 1)) || g.C < 32 || (path_policy() & 32)) return 0;
+        int m = encode_im2col(map, op.x, g.N, g.H, g.W, g.C, -g.ph, -g.pw, g.ph - (g.R - 1), g.pw - (g.S - 1), g.sh,
+                              g.sw, BK, g.C);
+        if (!m) return 0;
+        d.kcontig = 3;
+        d.cblk_log2 = __builtin_ctz(unsigned(g.C));
+        return 5;
     }
     cuuint64_t dims[2] = {cuuint64_t(op.g.C), cuuint64_t(op.Kd)};
     cuuint64_t st[1] = {cuuint64_t(op.g.C) * 4};

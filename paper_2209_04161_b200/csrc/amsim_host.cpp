@@ -180,7 +180,7 @@ uint64_t amsim_launch_count(void) { return g_launches.load(); }
 
 amsim_status amsim_set_path_policy(int policy)
 {
-    if (policy < 0 || policy > 31) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 31]");
+    if (policy < 0 || policy > 63) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 63]");
     g_policy.store(policy);
     return AMSIM_OK;
 }

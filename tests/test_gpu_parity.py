@@ -723,6 +723,35 @@ def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
         assert_bits(run_gemm(am, lut, A, B), orc.gemm(A, B, "mbm", 7).c32, "gemm")
 
 
+@pytest.mark.parametrize("force", [None, "1", "2", "12", "14", "15", "16"])
+def test_wgrad_multi_tap_tma(am, luts, orc, force, monkeypatch):
+    """wgrad activation tiles whose rows span several taps (rows a multiple of a
+    power-of-two C >= 32: one TMA im2col box per tap, smem tap-blocked; the
+    tap blocks past R*S*C are zero-filled) give the same bits as the cp.async
+    gather (policy bit 5) and the oracle's sequential order, in both
+    orientations, with ragged tap counts, strides, 5x5 taps and ragged pixels."""
+    lut = luts("mbm")
+    if force:
+        monkeypatch.setenv("AMSIM_FORCE_CFG", force)
+    shapes = [(2, 12, 12, 32, 48, 3, 3, 1, 1), (2, 11, 11, 64, 32, 3, 3, 2, 1), (2, 9, 9, 32, 40, 5, 5, 1, 2),
+              (1, 10, 10, 128, 24, 3, 3, 1, 1), (3, 7, 9, 64, 16, 3, 3, 1, 1)]
+    for k, shape in enumerate(shapes):
+        x, w, dy, OH, OW = _conv_tensors(shape, 170 + k)
+        d = am.conv_desc(*shape)
+        od = orc.conv_desc(*shape)
+        got = {}
+        for pol in (2, 2 | 32):
+            am.amsim_set_path_policy(pol)
+            try:
+                got[pol] = _run_conv(am, lut, d, x, w, dy, "wgrad")
+            finally:
+                am.amsim_set_path_policy(0)
+        want = orc.conv_bwd_filter(od, x, dy, "mbm")
+        assert_bits(got[2], want.c32, f"{shape} multi-tap TMA vs c32")
+        assert_bits(got[2 | 32], want.c32, f"{shape} cp.async vs c32")
+        assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), want, f"{shape} split")
+
+
 @pytest.mark.parametrize("force", [None, "14", "16", "6"])
 def test_gemm_accumulate_and_leading_dims_transposed(am, luts, orc, force, monkeypatch):
     """C += A B with padded leading dimensions in both orientations (the
