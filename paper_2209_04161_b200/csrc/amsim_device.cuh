@@ -399,8 +399,8 @@ struct DgDY {
         int h = g.sh * int(u) + P.ch, w = g.sw * int(v) + P.cw;
         return ((int64_t(n) * g.H + h) * g.W + w) * ldc;
     }
-    // TMA box origin (stride 1 only: one phase).  1x1 unpadded: dy as
-    // [pixels][K].  Otherwise im2col mode over dy (K % BK == 0): output pixel
+    // TMA box origin (stride 1: one phase; or 1x1 unpadded at any stride, whose
+    // only phase with a tap is (0, 0)).  1x1 unpadded: dy as [pixels][K].  Otherwise im2col mode over dy (K % BK == 0): output pixel
     // (n, h, w) has base (w + pw - (S-1), h + ph - (R-1), n) and tap (i, j) of the
     // reverse_transpose order reads dy[h + ph - kh] with kh = R-1-i: offsets (j, i).
     __device__ __forceinline__ void tma_coords(int s, int m0, int k0, int *c) const

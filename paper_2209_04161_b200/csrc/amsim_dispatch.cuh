@@ -96,6 +96,7 @@ using CfgWide = KCfg<256, 8, 4>;                         // N > 64, M <= 64
 using CfgHuge = KCfg<256, 16, 8>;                        // N >= 256, 16/32-bit tables (fewer operand loads per lookup)
 using CfgFlat = KCfg<256, 16, 4, 2>;                     // 64 x 256: 64-row problems (64-channel layers, transposed)
                                                          // with Big's 16 x 4 register tile instead of Wide's 8 x 4
+using CfgTall = KCfg<256, 20, 2>;                        // 160 x 64: 129..160-row problems (stem wgrad, M = 7*7*3)
 
 static int g_num_sms = 0;
 static int num_sms()
@@ -129,7 +130,7 @@ struct Problem {
     bool a_is_activation = false;
 };
 
-enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat };
+enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat, Tall };
 static constexpr size_t kSmemMax = 227 * 1024;
 
 static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t lut_bytes)
@@ -141,6 +142,7 @@ static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t
     case CfgId::Wide: BM = CfgWide::BM; BN = CfgWide::BN; NT = CfgWide::NT; smem = CfgWide::smem_bytes(lut_bytes); break;
     case CfgId::Huge: BM = CfgHuge::BM; BN = CfgHuge::BN; NT = CfgHuge::NT; smem = CfgHuge::smem_bytes(lut_bytes); break;
     case CfgId::Flat: BM = CfgFlat::BM; BN = CfgFlat::BN; NT = CfgFlat::NT; smem = CfgFlat::smem_bytes(lut_bytes); break;
+    case CfgId::Tall: BM = CfgTall::BM; BN = CfgTall::BN; NT = CfgTall::NT; smem = CfgTall::smem_bytes(lut_bytes); break;
     default: BM = CfgBig::BM; BN = CfgBig::BN; NT = CfgBig::NT; smem = CfgBig::smem_bytes(lut_bytes); break;
     }
 }
@@ -236,6 +238,7 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
     case CfgId::Wide: TM = 8; TN = 4; break;
     case CfgId::Huge: TM = 16; TN = 8; break;
     case CfgId::Flat: TM = 16; TN = 4; break;
+    case CfgId::Tall: TM = 20; TN = 2; break;
     default: break;
     }
     double row = double(size_t(1) << mbits) * (eb / 8);
@@ -315,6 +318,8 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     if (smem_table) {
         cands = {CfgId::Small, CfgId::Mid, CfgId::Big, CfgId::Lean, CfgId::Wide, CfgId::Flat};
         if (eb >= 16) cands.push_back(CfgId::Huge);
+        // one 160-row tile for 129..160 rows (Mid / Lean would pad 147 rows to 256 / 192)
+        if (pr.nsub == 1 && pr.M[0] > 128 && pr.M[0] <= CfgTall::BM) cands.push_back(CfgId::Tall);
     } else {
         cands = {CfgId::Big, CfgId::Lean};
     }
@@ -437,6 +442,7 @@ static amsim_status launch_eb(const KParams &p, const OpA &a, const OpB &b, cuda
     case CfgId::Lean: return launch_cfg<CfgLean, EB>(p, a, b, st);
     case CfgId::Wide: return launch_cfg<CfgWide, EB>(p, a, b, st);
     case CfgId::Flat: return launch_cfg<CfgFlat, EB>(p, a, b, st);
+    case CfgId::Tall: return launch_cfg<CfgTall, EB>(p, a, b, st);
     case CfgId::Huge:
         if constexpr (EB >= 16) return launch_cfg<CfgHuge, EB>(p, a, b, st);
         else return set_error(AMSIM_ERR_UNSUPPORTED, "internal: Huge tiles need 16/32-bit tables");
@@ -588,14 +594,16 @@ static int setup_tma(CUtensorMap *map, const WgX &op, int rows, OpDesc &d)
     return encode_tma(map, op.x, 2, dims, st, box, false);
 }
 
-// conv dgrad A: for 1x1 / stride 1 / unpadded (one phase), dy as [pixels][K];
+// conv dgrad A: for 1x1 / unpadded (any stride: one phase with a tap), dy as [pixels][K];
 // other stride-1 convs: im2col mode over dy (lower = pad - (R-1),
 // upper = pad - (R-1) + H - OH) when K % BK == 0
 static int setup_tma(CUtensorMap *map, const DgDY &op, int rows, OpDesc &d)
 {
     if (tma_disabled()) return 0;
     const ConvGeom &g = op.g;
-    if (!is_1x1_s1(op.g)) {
+    // 1x1 unpadded, any stride: only phase (0, 0) has a tap, and its rows are
+    // dy's pixels in order (Hp = OH, Wp = OW) -- the plain 2-D box below
+    if (!(g.R == 1 && g.S == 1 && g.ph == 0 && g.pw == 0)) {
         if (g.sh != 1 || g.sw != 1) return 0;
         int m = encode_im2col(map, op.dy, g.N, g.OH, g.OW, g.K, g.ph - (g.R - 1), g.pw - (g.S - 1),
                               g.ph - (g.R - 1) + g.H - g.OH, g.pw - (g.S - 1) + g.W - g.OW, 1, 1, rows);

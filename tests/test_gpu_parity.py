@@ -638,7 +638,8 @@ def test_exponent_cast_gemm_and_conv(am, luts, orc, e):
 def test_tma_staging_equals_cp_async(am, luts, orc):
     """Box-shaped operand tiles (GEMM A / B, conv fwd weights, wgrad errors,
     dgrad weight taps via 3-D maps, 1x1 / stride-1 activations and errors,
-    64-byte swizzled where k is contiguous) are loaded by TMA by default; the
+    1x1 strided errors (dgrad phase (0, 0)), 64-byte swizzled where k is
+    contiguous) are loaded by TMA by default; the
     bits equal the all-cp.async path and the oracle, including ragged
     M / N / K edges (TMA zero fill)."""
     lut = luts("mbm")
@@ -647,7 +648,8 @@ def test_tma_staging_equals_cp_async(am, luts, orc):
     At = np.ascontiguousarray(inp.normal((77, 132), 113))   # trans_a, lda = 132 -> TMA eligible A
     shapes = [(3, 13, 11, 12, 40, 3, 3, 2, 1), (2, 9, 7, 16, 48, 1, 1, 1, 0), (2, 8, 8, 12, 32, 3, 3, 1, 1),
               (2, 10, 10, 8, 64, 3, 3, 2, 1), (3, 9, 9, 32, 48, 3, 3, 1, 1), (2, 15, 15, 16, 32, 3, 3, 2, 1),
-              (2, 9, 9, 128, 64, 3, 3, 1, 1), (2, 12, 12, 64, 128, 3, 3, 2, 1)]
+              (2, 9, 9, 128, 64, 3, 3, 1, 1), (2, 12, 12, 64, 128, 3, 3, 2, 1), (2, 9, 7, 32, 48, 1, 1, 2, 0),
+              (3, 10, 12, 16, 64, 1, 1, 2, 0)]
     outs = {}
     for pol in (2, 10):
         am.amsim_set_path_policy(pol)
@@ -663,6 +665,10 @@ def test_tma_staging_equals_cp_async(am, luts, orc):
         assert_bits(outs[2][i], outs[10][i], f"part {i}")
     assert_bits(outs[2][0], orc.gemm(A, B, "mbm", 7).c32, "gemm vs c32")
     assert_bits(outs[2][1], orc.gemm(np.ascontiguousarray(At.T), B, "mbm", 7).c32, "gemm trans_a vs c32")
+    for k in (8, 9):   # 1x1 strided dgrad (TMA box of dy for phase (0, 0), zeros elsewhere) vs the oracle
+        x, w, dy, OH, OW = _conv_tensors(shapes[k], 114 + k)
+        want = orc.conv_bwd_data(orc.conv_desc(*shapes[k]), dy, w, "mbm").c32
+        assert_bits(outs[2][2 + 3 * k + 2], want, f"{shapes[k]} dgrad vs c32")
 
 
 # ---------------------------------------------------------------------------
@@ -750,6 +756,33 @@ def test_wgrad_multi_tap_tma(am, luts, orc, force, monkeypatch):
         assert_bits(got[2], want.c32, f"{shape} multi-tap TMA vs c32")
         assert_bits(got[2 | 32], want.c32, f"{shape} cp.async vs c32")
         assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), want, f"{shape} split")
+
+
+@pytest.mark.parametrize("model", ["mbm", "mitchell"])
+def test_tall_tiles_129_to_160_rows(am, luts, orc, model, monkeypatch):
+    """Problems of 129..160 rows (the stem's wgrad: M = 7*7*3 = 147) may use
+    the 160 x 64 Tall tiles (20 x 2 register tiles); forced (AMSIM_FORCE_CFG=7)
+    and automatic plans give the oracle's bits in exact order and meet the
+    tolerance with split-K, including ragged rows / columns and the C = 3
+    activation gather."""
+    lut = luts(model)
+    shape = (2, 20, 20, 3, 24, 7, 7, 2, 3)
+    x, w, dy, OH, OW = _conv_tensors(shape, 180)
+    d = am.conv_desc(*shape)
+    od = orc.conv_desc(*shape)
+    A = inp.normal((150, 333), 181)
+    B = inp.normal((333, 70), 182)
+    for force in ("7", None):
+        if force:
+            monkeypatch.setenv("AMSIM_FORCE_CFG", force)
+        else:
+            monkeypatch.delenv("AMSIM_FORCE_CFG", raising=False)
+        want = orc.conv_bwd_filter(od, x, dy, model)
+        with exact_order(am):
+            assert_bits(_run_conv(am, lut, d, x, w, dy, "wgrad"), want.c32, f"force={force} wgrad")
+            assert_bits(run_gemm(am, lut, A, B), orc.gemm(A, B, model, 7).c32, f"force={force} gemm")
+        assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), want, f"force={force} wgrad split")
+        assert_tol(run_gemm(am, lut, A, B), orc.gemm(A, B, model, 7), f"force={force} gemm split")
 
 
 @pytest.mark.parametrize("force", [None, "14", "16", "6"])
