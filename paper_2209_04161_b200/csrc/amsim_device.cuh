@@ -37,6 +37,9 @@ namespace dev {
 #ifndef AMSIM_PACK
 #define AMSIM_PACK 1
 #endif
+#ifndef AMSIM_SKIP
+#define AMSIM_SKIP 1
+#endif
 #ifndef AMSIM_PACK8
 #define AMSIM_PACK8 0
 #endif
@@ -148,6 +151,20 @@ __device__ __forceinline__ float add_ftz(float a, float b)
     float d;
     asm("add.rn.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
     return d;
+}
+
+// Shared-memory table entry at `addr`, loaded only when `act` != 0 (else `v`
+// keeps its previous value): a predicated-off LDS requests no shared-memory
+// wavefront.
+template <int EB>
+__device__ __forceinline__ void lut_entry_if(uint32_t &v, uint32_t addr, uint32_t act)
+{
+    if constexpr (EB == 16)
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u16 %0, [%1];\n\t}"
+                     : "+r"(v) : "r"(addr), "r"(act));
+    else
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
+                     : "+r"(v) : "r"(addr), "r"(act));
 }
 
 // Table entry at byte offset `addr`: a shared-memory address (GL = false) or
@@ -623,6 +640,13 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // issue-bound and loses more to the unpacking than it gains: measured
     // +5.7 % / -3.8 % on the ResNet-50 step)
     constexpr bool PK = AMSIM_PACK && MUL == MUL_LUT && !GL && (EB >= 16 || AMSIM_PACK8);
+    // Zero-row skipping (normal orientation, LSU-bound 16/32-bit shared tables):
+    // a warp-shared A element with a zero exponent field (+-0, subnormal) has
+    // alpha_a = +-0, so its products add +-0 to acc (never -0: it starts at +0)
+    // and leave it unchanged whatever the entry -- the lookup is predicated off
+    // (no wavefront) and the FFMA reuses the column's last entry, a valid table
+    // value, so x stays finite under the fast-path conditions.  Same bits.
+    constexpr bool SKIP = AMSIM_SKIP && MUL == MUL_LUT && !GL && EB >= 16 && !TRN;
     constexpr uint32_t AMASK = 0xFF800000u, OMASK = 0x007FFFFFu;
     extern __shared__ __align__(128) unsigned char smem[];
 
@@ -748,6 +772,9 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     for (int s = 0; s < STAGES - 1; s++) issue_next();
 
     float acc[TM][TN];
+    uint32_t ecur[TN];   // SKIP: last entry loaded per column
+#pragma unroll
+    for (int c = 0; c < TN; c++) ecur[c] = 0;
     int g = 0;
     for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
         const Tile T = tile_of(tile);
@@ -874,8 +901,14 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     for (int r = 0; r < TM; r++)
 #pragma unroll
                         for (int c = 0; c < TN; c++) {
-                            uint32_t e = MUL == MUL_LUT ? lut_entry<EB, GL>(aof[r] + bof[c], lut_g)
-                                                        : direct_entry<MUL>(aof[r], bof[c]);
+                            uint32_t e;
+                            if constexpr (SKIP) {
+                                lut_entry_if<EB>(ecur[c], aof[r] + bof[c], aal[r] << 1);
+                                e = ecur[c];
+                            } else {
+                                e = MUL == MUL_LUT ? lut_entry<EB, GL>(aof[r] + bof[c], lut_g)
+                                                   : direct_entry<MUL>(aof[r], bof[c]);
+                            }
                             uint32_t x = e * mul[c] + bal[c];
                             acc[r][c] = fma_ftz(__uint_as_float(x), __uint_as_float(aal[r]), acc[r][c]);
                         }

@@ -246,6 +246,16 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
     return lk + 1.0 / TN + 2.0 / TM;
 }
 
+static int cfg_tn(CfgId c)
+{
+    switch (c) {
+    case CfgId::Small: return 1;
+    case CfgId::Mid: case CfgId::Lean: case CfgId::Tall: return 2;
+    case CfgId::Huge: return 8;
+    default: return 4;
+    }
+}
+
 // Plan cache: the same problem (shape, table width, mode, policy) is planned
 // once per process.
 struct PlanRec {
@@ -344,6 +354,14 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         q.cfg = int(c);
         q.trn = 0;
         double cost = tile_plan(q, pr, BM, BN, policy) * double(BM) * BN * wf_per_lookup(c, eb, mbits, smem_table);
+        // zero-row skipping (SKIP in amsim_mm_kernel): in this orientation a layer
+        // input's zeros (ReLU) are warp-shared rows whose lookups are predicated
+        // off.  The saving grows with the columns per lane (the predicate and the
+        // operand loads are per row): measured on ResNet-50 (MBM, m = 7) at
+        // 0.87-0.89 of Huge^T for Huge (16 x 8), 0.96-1.04 for Big (16 x 4),
+        // none for 2-column tiles -- factors calibrated on those ratios.
+        if (pr.a_is_activation && AMSIM_SKIP && smem_table && eb >= 16 && p.mul == MUL_LUT)
+            cost *= cfg_tn(c) >= 8 ? 0.84 : cfg_tn(c) >= 4 ? 0.92 : 1.0;
         if (cost < best * 0.999) {
             best = cost;
             bestp = q;
