@@ -28,7 +28,11 @@ amsim_status amsim_conv2d_bwd_filter_workspace(const amsim_lut *lut, const amsim
     if (s != AMSIM_OK) return s;
     // The plan (hence the workspace) depends on the multiply mode and the
     // table layout policy; report the maximum so one allocation serves all.
+    // A variant with no plan (a forced tile configuration that only fits some
+    // table layouts, AMSIM_FORCE_CFG) is skipped; an error only if none plans.
     int64_t need = 0;
+    bool any = false;
+    amsim_status last = AMSIM_OK;
     const int pol = path_policy() & 3;   // bits 2 (table layout) and 4 (orientation) are varied below
     for (int mode : {AMSIM_MUL_LUT, AMSIM_MUL_NATIVE})
         for (int policy : {pol, pol | 4, pol | 16, pol | 4 | 16}) {
@@ -36,9 +40,15 @@ amsim_status amsim_conv2d_bwd_filter_workspace(const amsim_lut *lut, const amsim
             ConvGeom g;
             int eb;
             s = wgrad_plan(lut, d, p, g, eb, mode, policy);
-            if (s != AMSIM_OK) return s;
+            if (s != AMSIM_OK) {
+                last = s;
+                continue;
+            }
+            any = true;
             need = std::max<int64_t>(need, p.ws_elems);
         }
+    if (!any) return last;
+    clear_error();
     *bytes = size_t(need) * sizeof(float);
     return AMSIM_OK;
 }

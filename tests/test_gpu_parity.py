@@ -758,6 +758,42 @@ def test_wgrad_multi_tap_tma(am, luts, orc, force, monkeypatch):
         assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), want, f"{shape} split")
 
 
+@pytest.mark.parametrize("policy", [2 | 16, 2 | 16 | 4])
+def test_zero_row_skipping_bits(am, luts, orc, policy):
+    """Normal orientation (policy bit 4), 16- and 32-bit table layouts: warp-
+    shared A elements that are +0, -0 or subnormal (zero exponent field) have
+    their lookups predicated off; rows that start with zeros (no entry loaded
+    yet), alternate, or are all zero give the oracle's c32 bits, as do the
+    conv fwd / wgrad passes on ReLU activations."""
+    lut = luts("mbm")
+    g = inp.rng(190)
+    M, N, K = 300, 200, 150
+    A = inp.normal((M, K), 191)
+    z = g.random((M, K)) < 0.6
+    A[z] = 0.0
+    A[g.random((M, K)) < 0.05] = -0.0
+    sub = g.random((M, K)) < 0.03
+    A[sub] = (g.integers(1, 1 << 23, int(sub.sum())).astype(np.uint32)).view(np.float32)
+    A[:7, :] = 0.0           # all-zero rows
+    A[7:20, :40] = 0.0       # rows whose first k-tiles are all zero
+    A[:, ::5] = -0.0
+    B = inp.normal((K, N), 192)
+    shape = (2, 12, 12, 32, 64, 3, 3, 1, 1)
+    x, w, dy, OH, OW = _conv_tensors(shape, 193)
+    d = am.conv_desc(*shape)
+    od = orc.conv_desc(*shape)
+    am.amsim_set_path_policy(policy)
+    try:
+        got = run_gemm(am, lut, A, B)
+        fwd = _run_conv(am, lut, d, x, w, dy, "fwd")
+        wgr = _run_conv(am, lut, d, x, w, dy, "wgrad")
+    finally:
+        am.amsim_set_path_policy(0)
+    assert_bits(got, orc.gemm(A, B, "mbm", 7).c32, "gemm with zero / subnormal rows")
+    assert_bits(fwd, orc.conv_fwd(od, x, w, "mbm").c32, "fwd")
+    assert_bits(wgr, orc.conv_bwd_filter(od, x, dy, "mbm").c32, "wgrad")
+
+
 @pytest.mark.parametrize("model", ["mbm", "mitchell"])
 def test_tall_tiles_129_to_160_rows(am, luts, orc, model, monkeypatch):
     """Problems of 129..160 rows (the stem's wgrad: M = 7*7*3 = 147) may use
