@@ -646,7 +646,9 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // and leave it unchanged whatever the entry -- the lookup is predicated off
     // (no wavefront) and the FFMA reuses the column's last entry, a valid table
     // value, so x stays finite under the fast-path conditions.  Same bits.
-    constexpr bool SKIP = AMSIM_SKIP && MUL == MUL_LUT && !GL && EB >= 16 && !TRN;
+    // Only for TN >= 4: the per-row predicate costs one LOP3 per row and k,
+    // which 1- and 2-column tiles cannot amortise (LeNet-5: +17 % measured).
+    constexpr bool SKIP = AMSIM_SKIP && MUL == MUL_LUT && !GL && EB >= 16 && !TRN && TN >= 4;
     constexpr uint32_t AMASK = 0xFF800000u, OMASK = 0x007FFFFFu;
     extern __shared__ __align__(128) unsigned char smem[];
 

@@ -326,7 +326,14 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     // only); cost = planned makespan in k-tiles x lookups per k-tile x wavefronts per lookup.
     std::vector<CfgId> cands;
     if (smem_table) {
-        cands = {CfgId::Small, CfgId::Mid, CfgId::Big, CfgId::Lean, CfgId::Wide, CfgId::Flat};
+        cands = {CfgId::Small, CfgId::Mid, CfgId::Big, CfgId::Lean, CfgId::Flat};
+        // Wide (8 x 4) only for <= 64-row problems, its purpose: on larger ones the
+        // wavefront model under-prices its instruction overhead (7.3 instructions
+        // per approx-MAC vs 5.1 for 16 x 8, ncu) and it measured 5-18 % slower
+        // than Big / Huge on every ResNet-18 pass where it was picked
+        int mmax = 0;
+        for (int i = 0; i < pr.nsub; i++) mmax = std::max(mmax, pr.M[i]);
+        if (mmax <= 64) cands.push_back(CfgId::Wide);
         if (eb >= 16) cands.push_back(CfgId::Huge);
         // one 160-row tile for 129..160 rows (Mid / Lean would pad 147 rows to 256 / 192)
         if (pr.nsub == 1 && pr.M[0] > 128 && pr.M[0] <= CfgTall::BM) cands.push_back(CfgId::Tall);
