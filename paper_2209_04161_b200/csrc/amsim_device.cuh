@@ -40,6 +40,9 @@ namespace dev {
 #ifndef AMSIM_SKIP
 #define AMSIM_SKIP 1
 #endif
+#ifndef AMSIM_KK_UNROLL_SMALL
+#define AMSIM_KK_UNROLL_SMALL 2   // fast-path k unroll for register tiles of <= 64 products
+#endif
 #ifndef AMSIM_PACK8
 #define AMSIM_PACK8 0
 #endif
@@ -648,6 +651,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // value, so x stays finite under the fast-path conditions.  Same bits.
     // Only for TN >= 4: the per-row predicate costs one LOP3 per row and k,
     // which 1- and 2-column tiles cannot amortise (LeNet-5: +17 % measured).
+    constexpr int KK_UNROLL = TM * TN <= 64 ? AMSIM_KK_UNROLL_SMALL : 2;
     constexpr bool SKIP = AMSIM_SKIP && MUL == MUL_LUT && !GL && EB >= 16 && !TRN && TN >= 4;
     constexpr uint32_t AMASK = 0xFF800000u, OMASK = 0x007FFFFFu;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -853,7 +857,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                         for (int c = 0; c < TN; c++) acc[r][c] = __fmaf_rn(av[r], bv[c], acc[r][c]);
                 }
             } else if (fast) {
-#pragma unroll 2
+#pragma unroll KK_UNROLL
                 for (int kk = 0; kk < BK; kk++) {
                     uint32_t aal[TM], aof[TM], bal[TN], bof[TN], mul[TN];
 #pragma unroll
