@@ -96,7 +96,8 @@ using CfgWide = KCfg<256, 8, 4>;                         // N > 64, M <= 64
 using CfgHuge = KCfg<256, 16, 8>;                        // N >= 256, 16/32-bit tables (fewer operand loads per lookup)
 using CfgFlat = KCfg<256, 16, 4, 2>;                     // 64 x 256: 64-row problems (64-channel layers, transposed)
                                                          // with Big's 16 x 4 register tile instead of Wide's 8 x 4
-using CfgTall = KCfg<256, 20, 2>;                        // 160 x 64: 129..160-row problems (stem wgrad, M = 7*7*3)
+using CfgTall = KCfg<256, 20, 2>;
+using CfgFlat3 = KCfg<256, 16, 3, 2>;                    // 64 x 192, transposed only: lanes = 576 = 3 x 192 (3x3 x 64-channel wgrad)                        // 160 x 64: 129..160-row problems (stem wgrad, M = 7*7*3)
 
 static int g_num_sms = 0;
 static int num_sms()
@@ -130,7 +131,7 @@ struct Problem {
     bool a_is_activation = false;
 };
 
-enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat, Tall };
+enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat, Tall, Flat3 };
 static constexpr size_t kSmemMax = 227 * 1024;
 
 static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t lut_bytes)
@@ -143,6 +144,7 @@ static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t
     case CfgId::Huge: BM = CfgHuge::BM; BN = CfgHuge::BN; NT = CfgHuge::NT; smem = CfgHuge::smem_bytes(lut_bytes); break;
     case CfgId::Flat: BM = CfgFlat::BM; BN = CfgFlat::BN; NT = CfgFlat::NT; smem = CfgFlat::smem_bytes(lut_bytes); break;
     case CfgId::Tall: BM = CfgTall::BM; BN = CfgTall::BN; NT = CfgTall::NT; smem = CfgTall::smem_bytes(lut_bytes); break;
+    case CfgId::Flat3: BM = CfgFlat3::BM; BN = CfgFlat3::BN; NT = CfgFlat3::NT; smem = CfgFlat3::smem_bytes(lut_bytes); break;
     default: BM = CfgBig::BM; BN = CfgBig::BN; NT = CfgBig::NT; smem = CfgBig::smem_bytes(lut_bytes); break;
     }
 }
@@ -239,6 +241,7 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
     case CfgId::Huge: TM = 16; TN = 8; break;
     case CfgId::Flat: TM = 16; TN = 4; break;
     case CfgId::Tall: TM = 20; TN = 2; break;
+    case CfgId::Flat3: TM = 16; TN = 3; break;
     default: break;
     }
     double row = double(size_t(1) << mbits) * (eb / 8);
@@ -251,6 +254,7 @@ static int cfg_tn(CfgId c)
     switch (c) {
     case CfgId::Small: return 1;
     case CfgId::Mid: case CfgId::Lean: case CfgId::Tall: return 2;
+    case CfgId::Flat3: return 3;
     case CfgId::Huge: return 8;
     default: return 4;
     }
@@ -384,6 +388,9 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         pt.N = pr.M[0];
         pt.M[0] = pr.N;
         std::vector<CfgId> tc = {CfgId::Wide, CfgId::Big, CfgId::Flat};
+        // 192 lanes where they tile the lane dimension exactly and 256 would not
+        // (3x3 x 64-channel wgrad: 576 = 3 x 192, vs 768 = 3 x 256 for Flat)
+        if (pr.M[0] % CfgFlat3::BN == 0 && pr.M[0] % CfgFlat::BN != 0) tc.push_back(CfgId::Flat3);
         if (eb >= 16) tc.push_back(CfgId::Huge);
         if (force >= 10) tc = {CfgId(force - 10)};
         if (force >= 10 && CfgId(force - 10) == CfgId::Huge && eb < 16) tc = {CfgId::Big};
@@ -664,6 +671,7 @@ static amsim_status launch_trn(const KParams &p, const OpR &r, const OpC &c, cud
     switch (CfgId(p.cfg)) {
     case CfgId::Wide: return launch_cfg<CfgWide, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Flat: return launch_cfg<CfgFlat, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
+    case CfgId::Flat3: return launch_cfg<CfgFlat3, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Big: return launch_cfg<CfgBig, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Huge:
         if constexpr (EB >= 16) return launch_cfg<CfgHuge, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);

@@ -704,7 +704,7 @@ def test_transposed_orientation_equals_normal(am, luts, orc, model):
     assert_tol(outs[16][0], res, "gemm split, normal orientation")
 
 
-@pytest.mark.parametrize("force", ["14", "12", "15", "16", "6"])
+@pytest.mark.parametrize("force", ["14", "12", "15", "16", "18", "6"])
 def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
     """Every pass in the transposed orientation (AMSIM_FORCE_CFG >= 10 forces
     it wherever it is allowed), cp.async operand gathers (C % BN != 0) and TMA
@@ -729,7 +729,7 @@ def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
         assert_bits(run_gemm(am, lut, A, B), orc.gemm(A, B, "mbm", 7).c32, "gemm")
 
 
-@pytest.mark.parametrize("force", [None, "1", "2", "12", "14", "15", "16"])
+@pytest.mark.parametrize("force", [None, "1", "2", "12", "14", "15", "16", "18"])
 def test_wgrad_multi_tap_tma(am, luts, orc, force, monkeypatch):
     """wgrad activation tiles whose rows span several taps (rows a multiple of a
     power-of-two C >= 32: one TMA im2col box per tap, smem tap-blocked; the
