@@ -494,9 +494,11 @@ struct KCfg {
     static constexpr __host__ __device__ int wrow(int w) { return (w / WN) * TM; }
     static constexpr __host__ __device__ int wcol(int w) { return (w % WN) * 32 * TN; }
     // a lane owns columns lane * CG + col(c), c < TN: groups of 4 consecutive
-    // columns 128 apart when TN >= 4 (conflict-free LDS.128), else TN consecutive
-    static constexpr int CG = TN >= 4 ? 4 : TN;
-    static constexpr __host__ __device__ int col(int c) { return TN >= 4 ? (c >> 2) * 128 + (c & 3) : c; }
+    // columns 128 apart when TN is a multiple of 4 (conflict-free LDS.128), else
+    // TN consecutive (TN = 2, 3, 5: scalar loads at an odd or 2-word lane stride)
+    static constexpr bool G4 = TN % 4 == 0;
+    static constexpr int CG = G4 ? 4 : TN;
+    static constexpr __host__ __device__ int col(int c) { return G4 ? (c >> 2) * 128 + (c & 3) : c; }
     static constexpr int RAW_A = BM * (BK + RAW_PAD);
     static constexpr int RAW_B = BN * (BK + RAW_PAD);
     static constexpr int RAW_STAGE = RAW_A + RAW_B;        // floats

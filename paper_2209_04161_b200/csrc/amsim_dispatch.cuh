@@ -97,6 +97,7 @@ using CfgHuge = KCfg<256, 16, 8>;                        // N >= 256, 16/32-bit 
 using CfgFlat = KCfg<256, 16, 4, 2>;                     // 64 x 256: 64-row problems (64-channel layers, transposed)
                                                          // with Big's 16 x 4 register tile instead of Wide's 8 x 4
 using CfgTall = KCfg<256, 20, 2>;
+using CfgTallT = KCfg<256, 8, 5>;                        // 64 x 160, transposed only: 129..160 lanes (stem wgrad, 147)
 using CfgFlat3 = KCfg<256, 16, 3, 2>;                    // 64 x 192, transposed only: lanes = 576 = 3 x 192 (3x3 x 64-channel wgrad)                        // 160 x 64: 129..160-row problems (stem wgrad, M = 7*7*3)
 
 static int g_num_sms = 0;
@@ -131,7 +132,7 @@ struct Problem {
     bool a_is_activation = false;
 };
 
-enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat, Tall, Flat3 };
+enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat, Tall, Flat3, TallT };
 static constexpr size_t kSmemMax = 227 * 1024;
 
 static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t lut_bytes)
@@ -144,6 +145,7 @@ static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t
     case CfgId::Huge: BM = CfgHuge::BM; BN = CfgHuge::BN; NT = CfgHuge::NT; smem = CfgHuge::smem_bytes(lut_bytes); break;
     case CfgId::Flat: BM = CfgFlat::BM; BN = CfgFlat::BN; NT = CfgFlat::NT; smem = CfgFlat::smem_bytes(lut_bytes); break;
     case CfgId::Tall: BM = CfgTall::BM; BN = CfgTall::BN; NT = CfgTall::NT; smem = CfgTall::smem_bytes(lut_bytes); break;
+    case CfgId::TallT: BM = CfgTallT::BM; BN = CfgTallT::BN; NT = CfgTallT::NT; smem = CfgTallT::smem_bytes(lut_bytes); break;
     case CfgId::Flat3: BM = CfgFlat3::BM; BN = CfgFlat3::BN; NT = CfgFlat3::NT; smem = CfgFlat3::smem_bytes(lut_bytes); break;
     default: BM = CfgBig::BM; BN = CfgBig::BN; NT = CfgBig::NT; smem = CfgBig::smem_bytes(lut_bytes); break;
     }
@@ -242,6 +244,7 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
     case CfgId::Flat: TM = 16; TN = 4; break;
     case CfgId::Tall: TM = 20; TN = 2; break;
     case CfgId::Flat3: TM = 16; TN = 3; break;
+    case CfgId::TallT: TM = 8; TN = 5; break;
     default: break;
     }
     double row = double(size_t(1) << mbits) * (eb / 8);
@@ -255,6 +258,7 @@ static int cfg_tn(CfgId c)
     case CfgId::Small: return 1;
     case CfgId::Mid: case CfgId::Lean: case CfgId::Tall: return 2;
     case CfgId::Flat3: return 3;
+    case CfgId::TallT: return 5;
     case CfgId::Huge: return 8;
     default: return 4;
     }
@@ -391,6 +395,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         // 192 lanes where they tile the lane dimension exactly and 256 would not
         // (3x3 x 64-channel wgrad: 576 = 3 x 192, vs 768 = 3 x 256 for Flat)
         if (pr.M[0] % CfgFlat3::BN == 0 && pr.M[0] % CfgFlat::BN != 0) tc.push_back(CfgId::Flat3);
+        if (pr.M[0] > 128 && pr.M[0] <= CfgTallT::BN) tc.push_back(CfgId::TallT);
         if (eb >= 16) tc.push_back(CfgId::Huge);
         if (force >= 10) tc = {CfgId(force - 10)};
         if (force >= 10 && CfgId(force - 10) == CfgId::Huge && eb < 16) tc = {CfgId::Big};
@@ -672,6 +677,7 @@ static amsim_status launch_trn(const KParams &p, const OpR &r, const OpC &c, cud
     case CfgId::Wide: return launch_cfg<CfgWide, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Flat: return launch_cfg<CfgFlat, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Flat3: return launch_cfg<CfgFlat3, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
+    case CfgId::TallT: return launch_cfg<CfgTallT, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Big: return launch_cfg<CfgBig, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Huge:
         if constexpr (EB >= 16) return launch_cfg<CfgHuge, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);

@@ -704,7 +704,7 @@ def test_transposed_orientation_equals_normal(am, luts, orc, model):
     assert_tol(outs[16][0], res, "gemm split, normal orientation")
 
 
-@pytest.mark.parametrize("force", ["14", "12", "15", "16", "18", "6"])
+@pytest.mark.parametrize("force", ["14", "12", "15", "16", "18", "19", "6"])
 def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
     """Every pass in the transposed orientation (AMSIM_FORCE_CFG >= 10 forces
     it wherever it is allowed), cp.async operand gathers (C % BN != 0) and TMA
@@ -808,7 +808,7 @@ def test_tall_tiles_129_to_160_rows(am, luts, orc, model, monkeypatch):
     od = orc.conv_desc(*shape)
     A = inp.normal((150, 333), 181)
     B = inp.normal((333, 70), 182)
-    for force in ("7", None):
+    for force in ("7", "19", None):
         if force:
             monkeypatch.setenv("AMSIM_FORCE_CFG", force)
         else:
