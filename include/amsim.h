@@ -221,9 +221,10 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
  *   bit 4 -- never use the transposed kernel orientation (default: for a
  *            symmetric table and N << M the planner may make the output
  *            channels the warp-shared rows; same bits);
- *   bit 5 -- gather wgrad activation tiles that span several taps with
- *            cp.async (default: when the tile's rows are a multiple of a
- *            power-of-two C >= 32, one TMA im2col box per tap).
+ *   bit 5 -- gather with cp.async the operand tiles that need several im2col
+ *            descriptors or boxes (default TMA: wgrad activation tiles spanning
+ *            taps of a power-of-two C >= 32, one box per tap; stride-2 dgrad
+ *            error tiles, one descriptor per stride phase).
  * Errors: AMSIM_ERR_INVALID_ARG outside [0, 63]. */
 amsim_status amsim_set_path_policy(int policy);
 

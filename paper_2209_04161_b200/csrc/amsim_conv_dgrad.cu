@@ -31,6 +31,12 @@ amsim_status amsim_conv2d_bwd_data(const amsim_lut *lut, const amsim_conv2d_desc
     int eb = 32;
     s = prepare(lut, p, pr, eb);
     if (s != AMSIM_OK) return s;
+    if (d->stride_h > 1 || d->stride_w > 1) {   // per-phase im2col TMA descriptors for the dy tiles
+        int BM, BN, NT;
+        size_t smem;
+        cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, 0);
+        a.ph_tma = encode_dgrad_phases(a, pr.nsub, p.trn ? BN : BM) ? 1 : 0;
+    }
     bool v = d->K % 4 == 0;
     p.da = OpDesc{1, (v && aligned16(dy)) ? 2 : 0};
     p.db = OpDesc{1, (v && aligned16(w)) ? 2 : 0};

@@ -388,11 +388,15 @@ struct WgX {
 struct DgPhase {
     int a, b, ch, cw;     // phase and first output row / column of the phase
     int th, tw;           // valid taps per axis
+    int lo_h, lo_w;       // dy row / column read by the phase's output (0, 0) at its tap offset 0 (im2col lower corner)
     int Hp, Wp;           // output rows / columns of the phase
     FastDiv fHpWp, fWp, fTwK;
 };
 
+constexpr int MAX_PH_TMA = 4;   // stride-2 dgrad: one im2col descriptor per phase
 struct DgDY {
+    CUtensorMap ph_map[MAX_PH_TMA];   // per-phase im2col descriptors (strided dgrad, TMA mode 6)
+    int ph_tma;                       // ph_map encoded for every phase with taps
     const float *dy;
     ConvGeom g;
     DgPhase ph[MAX_SUB];
@@ -419,8 +423,9 @@ struct DgDY {
         int h = g.sh * int(u) + P.ch, w = g.sw * int(v) + P.cw;
         return ((int64_t(n) * g.H + h) * g.W + w) * ldc;
     }
-    // TMA box origin (stride 1: one phase; or 1x1 unpadded at any stride, whose
-    // only phase with a tap is (0, 0)).  1x1 unpadded: dy as [pixels][K].  Otherwise im2col mode over dy (K % BK == 0): output pixel
+    // TMA box origin (stride 1: one phase; 1x1 unpadded at any stride, whose
+    // only phase with a tap is (0, 0); stride 2: one im2col descriptor per phase,
+    // ph_map[s], mode 6).  1x1 unpadded: dy as [pixels][K].  Otherwise im2col mode over dy (K % BK == 0): output pixel
     // (n, h, w) has base (w + pw - (S-1), h + ph - (R-1), n) and tap (i, j) of the
     // reverse_transpose order reads dy[h + ph - kh] with kh = R-1-i: offsets (j, i).
     __device__ __forceinline__ void tma_coords(int s, int m0, int k0, int *c) const
@@ -437,8 +442,8 @@ struct DgDY {
         uint32_t i = P.fTwK.div(uint32_t(k0)), r2 = uint32_t(k0) - i * uint32_t(P.tw * g.K);
         uint32_t j = fK.div(r2), co = r2 - j * g.K;
         c[0] = int(co);
-        c[1] = int(w) + g.pw - (g.S - 1);
-        c[2] = int(h) + g.ph - (g.R - 1);
+        c[1] = int(w) + P.lo_w;   // stride 1: pw - (S-1)
+        c[2] = int(h) + P.lo_h;   // stride 1: ph - (R-1)
         c[3] = int(n);
         c[4] = int(j);
         c[5] = int(i);
@@ -510,6 +515,12 @@ struct KCfg {
                8 * STAGES + 128;
     }
 };
+
+// Descriptor of sub-problem s: the operand's own per-phase map (DgDY, mode 6)
+// or the launch-wide one.
+template <class Op>
+__device__ __forceinline__ const CUtensorMap *phase_map(const Op &, int, const CUtensorMap *dflt) { return dflt; }
+__device__ __forceinline__ const CUtensorMap *phase_map(const DgDY &op, int s, const CUtensorMap *) { return &op.ph_map[s]; }
 
 template <int NT, int ROWS, class Op>
 __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, float *raw, int s, int mn0, int k0,
@@ -751,7 +762,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     // mode 5: one im2col box of 2^cblk_log2 channels per tap block of the tile
                     auto load_op = [&](int mode, const CUtensorMap *map, uint32_t dst, const auto &op, int mn0,
                                        int rows, int cbl) {
-                        if (mode == 5) {
+                        if (mode == 6) {   // per-phase im2col descriptor held by the operand map
+                            op.tma_coords(IT.s, mn0, k0, c);
+                            load(4, phase_map(op, IT.s, map), dst);
+                        } else if (mode == 5) {
                             for (int t = 0; t < (rows >> cbl); t++) {
                                 op.tma_coords(IT.s, mn0 + (t << cbl), k0, c);
                                 load(4, map, dst + uint32_t(t * (BK << cbl)) * 4u);

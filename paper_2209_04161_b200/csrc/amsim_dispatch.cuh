@@ -641,7 +641,11 @@ static int setup_tma(CUtensorMap *map, const DgDY &op, int rows, OpDesc &d)
     // 1x1 unpadded, any stride: only phase (0, 0) has a tap, and its rows are
     // dy's pixels in order (Hp = OH, Wp = OW) -- the plain 2-D box below
     if (!(g.R == 1 && g.S == 1 && g.ph == 0 && g.pw == 0)) {
-        if (g.sh != 1 || g.sw != 1) return 0;
+        if (g.sh != 1 || g.sw != 1) {   // per-phase descriptors encoded by the entry point (encode_dgrad_phases)
+            if (!op.ph_tma) return 0;
+            d.kcontig = 2;
+            return 6;
+        }
         int m = encode_im2col(map, op.dy, g.N, g.OH, g.OW, g.K, g.ph - (g.R - 1), g.pw - (g.S - 1),
                               g.ph - (g.R - 1) + g.H - g.OH, g.pw - (g.S - 1) + g.W - g.OW, 1, 1, rows);
         if (m) d.kcontig = 2;
@@ -653,6 +657,25 @@ static int setup_tma(CUtensorMap *map, const DgDY &op, int rows, OpDesc &d)
     int m = encode_tma(map, op.dy, 2, dims, st, box, true);
     if (m) d.kcontig = 2;
     return m;
+}
+
+// Strided dgrad (2 x 2 phases): one im2col descriptor over dy per phase with
+// lower corner (lo_h, lo_w) and upper = lower + (Hp, Wp) - (OH, OW), so the box
+// walks the phase's Hp x Wp output pixels and the tap offsets (j, i) reach the
+// dy pixels of the phase's taps (reverse_transpose order, as for stride 1).
+// Returns false (cp.async gathers) when any phase cannot be encoded.
+static bool encode_dgrad_phases(DgDY &op, int nsub, int rows)
+{
+    const ConvGeom &g = op.g;
+    if (tma_disabled() || (path_policy() & 32) || nsub > MAX_PH_TMA || g.K % BK) return false;
+    for (int s = 0; s < nsub; s++) {
+        const DgPhase &P = op.ph[s];
+        if (P.th == 0 || P.tw == 0 || P.Hp == 0 || P.Wp == 0) continue;   // no k-tiles / rows: never loaded
+        if (!encode_im2col(&op.ph_map[s], op.dy, g.N, g.OH, g.OW, g.K, P.lo_h, P.lo_w, P.lo_h + P.Hp - g.OH,
+                           P.lo_w + P.Wp - g.OW, 1, 1, rows))
+            return false;
+    }
+    return true;
 }
 
 // conv dgrad B: the reverse-transposed weight taps, a 3-D box {co, ci, tap} of w
@@ -787,6 +810,9 @@ static void dgrad_phases(const amsim_conv2d_desc *d, Problem &pr, DgPhase *ph)
             P.fHpWp.init(uint32_t(std::max(1, P.Hp * P.Wp)));
             P.fWp.init(uint32_t(std::max(1, P.Wp)));
             P.fTwK.init(uint32_t(std::max(1, P.tw * d->K)));
+            // dy row read by output row u at tap offset i: u + lo_h + i, lo_h = (ch + ph - a) / sh - (th - 1)
+            P.lo_h = (P.ch + d->pad_h - a) / sh - (P.th - 1);
+            P.lo_w = (P.cw + d->pad_w - b) / sw - (P.tw - 1);
             pr.M[a * sw + b] = d->N * P.Hp * P.Wp;
             pr.K[a * sw + b] = P.th * P.tw * d->K;
         }
