@@ -758,6 +758,33 @@ def test_wgrad_multi_tap_tma(am, luts, orc, force, monkeypatch):
         assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), want, f"{shape} split")
 
 
+@pytest.mark.parametrize("force", [None, "2", "5", "16", "15"])
+def test_strided_dgrad_phase_tma(am, luts, orc, force, monkeypatch):
+    """Stride-2 dgrad reads dy through one im2col TMA descriptor per stride
+    phase (lower corner from the phase's first tap, upper from its extent):
+    the oracle's bits in exact order and the cp.async gather's (policy bit 5),
+    odd and even sizes, pads 0..2, 3x3 / 5x5 / 2x2 / 1x3 kernels, both
+    orientations."""
+    if force:
+        monkeypatch.setenv("AMSIM_FORCE_CFG", force)
+    lut = luts("mbm")
+    shapes = [(2, 14, 14, 16, 32, 3, 3, 2, 1), (2, 13, 11, 8, 48, 3, 3, 2, 1), (2, 15, 15, 16, 16, 5, 5, 2, 2),
+              (3, 10, 12, 12, 32, 2, 2, 2, 0), (2, 9, 9, 24, 16, 1, 3, 2, 0), (2, 11, 11, 32, 64, 3, 3, 2, 0)]
+    for k, shape in enumerate(shapes):
+        x, w, dy, OH, OW = _conv_tensors(shape, 210 + k)
+        d = am.conv_desc(*shape)
+        want = orc.conv_bwd_data(orc.conv_desc(*shape), dy, w, "mbm")
+        got = {}
+        for pol in (2, 2 | 32):
+            am.amsim_set_path_policy(pol)
+            try:
+                got[pol] = _run_conv(am, lut, d, x, w, dy, "dgrad")
+            finally:
+                am.amsim_set_path_policy(0)
+            assert_bits(got[pol], want.c32, f"{shape} dgrad policy {pol}")
+        assert_tol(_run_conv(am, lut, d, x, w, dy, "dgrad"), want, f"{shape} dgrad split")
+
+
 @pytest.mark.parametrize("policy", [2 | 16, 2 | 16 | 4])
 def test_zero_row_skipping_bits(am, luts, orc, policy):
     """Normal orientation (policy bit 4), 16- and 32-bit table layouts: warp-
