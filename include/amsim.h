@@ -78,7 +78,9 @@ typedef float (*amsim_mul_fn)(float a, float b);
 
 /* Opaque LUT handle.  Immutable after creation; safe to share between host
  * threads and to use on several devices (each device gets its own copy,
- * uploaded lazily under a mutex on first use). */
+ * uploaded lazily under a mutex on first use; the upload is a synchronous
+ * host operation on a private stream, so a first call made inside a CUDA graph
+ * capture works and the graph contains only the compute launches). */
 typedef struct amsim_lut amsim_lut;
 
 /* Alg. 1.  For every (k, j) in [0, 2^m)^2 the probe
@@ -205,7 +207,8 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
 /* ---------------------------------------------------------------------- */
 /* Test and measurement hooks                                               */
 
-/* Execution policy (process-wide bit set, default 0):
+/* Execution policy (bit set of the CALLING THREAD, default 0; other threads'
+ * calls are unaffected):
  *   bit 0 -- force the literal Alg. 2 careful path everywhere (default: per
  *            smem tile, the FTZ fast path when the tile's exponent ranges make
  *            it bit-identical to Alg. 2, else the careful path);
@@ -228,7 +231,7 @@ amsim_status amsim_conv2d_bwd_filter(const amsim_lut *lut, const amsim_conv2d_de
  * Errors: AMSIM_ERR_INVALID_ARG outside [0, 63]. */
 amsim_status amsim_set_path_policy(int policy);
 
-/* Multiply mode (process-wide, default AMSIM_MUL_LUT).  The two other modes
+/* Multiply mode (of the calling thread, default AMSIM_MUL_LUT).  The two other modes
  * are measurement instruments for the paper's comparisons, not AMSim:
  *   AMSIM_MUL_LUT    -- AMSim: the table lookup of Alg. 2 (the product path);
  *   AMSIM_MUL_NATIVE -- the same GEMM / conv kernels with the native IEEE FP32

@@ -85,12 +85,16 @@ amsim_status amsim_avgpool_bwd(const float *dy, int32_t N, int32_t HW, int32_t C
 
 /* Softmax cross-entropy over K classes, mean over the N rows, fused with its
  * gradient: loss[0] = mean_n (logsumexp(z_n) - z_n[label_n]),
- * dz = (softmax(z) - onehot(label)) / N.  labels int32 in [0, K); the labels
+ * dz = (softmax(z) - onehot(label)) / D with D = grad_denominator, or N when
+ * it is 0.  Data-parallel training passes the GLOBAL batch as D, so the
+ * all-reduce SUM of the ranks' gradients is the gradient of the global-batch
+ * mean loss even with uneven shards.  labels int32 in [0, K); the labels
  * live on the device, so a row with an out-of-range label is not reported: it
- * contributes zero loss and the plain softmax / N gradient.
- * ws >= amsim_nn_workspace_bytes(N, 1). */
-amsim_status amsim_softmax_xent(const float *logits, const int32_t *labels, int32_t N, int32_t K, float *loss,
-                                float *dlogits, void *ws, size_t ws_bytes, amsim_stream_t stream);
+ * contributes zero loss and the plain softmax / D gradient.
+ * ws >= amsim_nn_workspace_bytes(N, 1).  AMSIM_ERR_INVALID_ARG if D < 0. */
+amsim_status amsim_softmax_xent(const float *logits, const int32_t *labels, int32_t N, int32_t K,
+                                int32_t grad_denominator, float *loss, float *dlogits, void *ws, size_t ws_bytes,
+                                amsim_stream_t stream);
 
 /* out = a + b over n elements (the residual-path gradient sum). */
 amsim_status amsim_add(const float *a, const float *b, float *out, int64_t n, amsim_stream_t stream);

@@ -113,7 +113,7 @@ def lib():
     L.amsim_maxpool_bwd.argtypes = [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp]
     L.amsim_avgpool_fwd.argtypes = [vp, i32, i32, i32, vp, vp]
     L.amsim_avgpool_bwd.argtypes = [vp, i32, i32, i32, vp, vp]
-    L.amsim_softmax_xent.argtypes = [vp, vp, i32, i32, vp, vp, vp, sz, vp]
+    L.amsim_softmax_xent.argtypes = [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]
     L.amsim_add.argtypes = [vp, vp, vp, i64, vp]
     L.amsim_sgd_momentum.argtypes = [vp, vp, vp, i64, f32, f32, f32, vp]
     _lib = L
@@ -264,15 +264,37 @@ def amsim_gemm(lut: Lut, A, B, C, trans_a: bool = False, trans_b: bool = False, 
     return C
 
 
+def _conv_ptr(t, name, numel):
+    """Device pointer of a conv operand after the checks the C ABI cannot make
+    (it sees only a pointer): float32, on the current CUDA device, contiguous,
+    and exactly the element count the descriptor implies."""
+    p = _dptr(t, name)
+    torch = _T()
+    if t.device.index != torch.cuda.current_device():
+        raise ValueError(f"{name} is on {t.device}, not the current device cuda:{torch.cuda.current_device()}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (NHWC / HWIO)")
+    if t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements; the descriptor needs {numel}")
+    return p
+
+
+def _conv_sizes(d: ConvDesc):
+    """Element counts of x, w, y for descriptor d."""
+    return d.N * d.H * d.W * d.C, d.R * d.S * d.C * d.K, d.N * d.OH * d.OW * d.K
+
+
 def amsim_conv2d_fwd(lut: Lut, d: ConvDesc, x, w, y, stream=None):
-    _check(lib().amsim_conv2d_fwd(lut.handle, ctypes.byref(d), _dptr(x, "x"), _dptr(w, "w"), _dptr(y, "y"),
-                                  _stream(stream)), "amsim_conv2d_fwd")
+    nx, nw, ny = _conv_sizes(d)
+    _check(lib().amsim_conv2d_fwd(lut.handle, ctypes.byref(d), _conv_ptr(x, "x", nx), _conv_ptr(w, "w", nw),
+                                  _conv_ptr(y, "y", ny), _stream(stream)), "amsim_conv2d_fwd")
     return y
 
 
 def amsim_conv2d_bwd_data(lut: Lut, d: ConvDesc, dy, w, dx, stream=None):
-    _check(lib().amsim_conv2d_bwd_data(lut.handle, ctypes.byref(d), _dptr(dy, "dy"), _dptr(w, "w"),
-                                       _dptr(dx, "dx"), _stream(stream)), "amsim_conv2d_bwd_data")
+    nx, nw, ny = _conv_sizes(d)
+    _check(lib().amsim_conv2d_bwd_data(lut.handle, ctypes.byref(d), _conv_ptr(dy, "dy", ny), _conv_ptr(w, "w", nw),
+                                       _conv_ptr(dx, "dx", nx), _stream(stream)), "amsim_conv2d_bwd_data")
     return dx
 
 
@@ -285,8 +307,11 @@ def amsim_conv2d_bwd_filter_workspace(lut: Lut, d: ConvDesc) -> int:
 
 def amsim_conv2d_bwd_filter(lut: Lut, d: ConvDesc, x, dy, dw, workspace=None, stream=None):
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().amsim_conv2d_bwd_filter(lut.handle, ctypes.byref(d), _dptr(x, "x"), _dptr(dy, "dy"),
-                                         _dptr(dw, "dw"),
+    if workspace is not None and (not workspace.is_cuda or not workspace.is_contiguous()):
+        raise ValueError("workspace must be a contiguous CUDA tensor")
+    nx, nw, ny = _conv_sizes(d)
+    _check(lib().amsim_conv2d_bwd_filter(lut.handle, ctypes.byref(d), _conv_ptr(x, "x", nx), _conv_ptr(dy, "dy", ny),
+                                         _conv_ptr(dw, "dw", nw),
                                          None if workspace is None else ctypes.c_void_p(workspace.data_ptr()),
                                          ws_bytes, _stream(stream)), "amsim_conv2d_bwd_filter")
     return dw
@@ -389,9 +414,10 @@ def amsim_avgpool_bwd(dy, N, HW, C, dx, stream=None):
     _check(lib().amsim_avgpool_bwd(_p(dy), N, HW, C, _p(dx), _stream(stream)), "amsim_avgpool_bwd")
 
 
-def amsim_softmax_xent(logits, labels, N, K, loss, dlogits, ws, stream=None):
+def amsim_softmax_xent(logits, labels, N, K, loss, dlogits, ws, grad_denominator=0, stream=None):
     w, wb = _ws(ws)
-    _check(lib().amsim_softmax_xent(_p(logits), _p(labels), N, K, _p(loss), _p(dlogits), w, wb, _stream(stream)),
+    _check(lib().amsim_softmax_xent(_p(logits), _p(labels), N, K, int(grad_denominator), _p(loss), _p(dlogits), w, wb,
+                                    _stream(stream)),
            "amsim_softmax_xent")
 
 

@@ -273,6 +273,7 @@ struct PlanRec {
 };
 static std::mutex g_plan_mu;
 static std::map<std::vector<int64_t>, PlanRec> g_plans;
+static constexpr size_t kPlanCacheMax = 4096;
 
 // Table, tile configuration and split plan for a problem.
 // mode / policy < 0: the process-wide multiply mode / path policy.
@@ -312,8 +313,10 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     const uint32_t smem_lut = smem_table ? bytes : 0u;
     int force = -1;   // AMSIM_FORCE_CFG: tuning experiments only (>= 10: transposed orientation, cfg - 10)
     if (const char *f = std::getenv("AMSIM_FORCE_CFG"); f && *f) force = std::atoi(f);
+    // lut->symmetric decides whether the transposed orientation (which reads
+    // LUT^T) may be planned, so it is part of the key
     std::vector<int64_t> key = {pr.N, pr.nsub, pr.max_splits, pr.a_is_activation, eb, p.lut_global, p.mul, policy & (3 | 16), mbits,
-                                num_sms(), force};
+                                num_sms(), force, lut->symmetric ? 1 : 0};
     for (int i = 0; i < pr.nsub; i++) {
         key.push_back(pr.M[i]);
         key.push_back(pr.K[i]);
@@ -425,6 +428,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     r.cfg = p.cfg; r.trn = p.trn; r.tiles_n = p.tiles_n; r.nsub = p.nsub; r.ntiles = p.ntiles; r.ws_elems = p.ws_elems;
     std::memcpy(r.sub, p.sub, sizeof(r.sub));
     std::lock_guard<std::mutex> g(g_plan_mu);
+    if (g_plans.size() >= kPlanCacheMax) g_plans.clear();   // bounded: a process planning many shapes re-plans
     g_plans.emplace(std::move(key), r);
     return AMSIM_OK;
 }

@@ -16,8 +16,10 @@ namespace amsim {
 
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
-static std::atomic<int> g_policy{0};
-static std::atomic<int> g_mul_mode{0};
+// path policy and multiply mode are per calling thread: a test hook on one
+// thread never changes the arithmetic of another thread's calls
+static thread_local int g_policy = 0;
+static thread_local int g_mul_mode = 0;
 
 amsim_status set_error(amsim_status s, const std::string &msg)
 {
@@ -29,9 +31,9 @@ void clear_error() { g_last_error.clear(); }
 
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-int path_policy() { return g_policy.load(std::memory_order_relaxed); }
+int path_policy() { return g_policy; }
 
-int multiply_mode() { return g_mul_mode.load(std::memory_order_relaxed); }
+int multiply_mode() { return g_mul_mode; }
 
 static inline uint32_t bits(float f)
 {
@@ -108,12 +110,22 @@ static amsim_status upload(amsim_lut *lut, int dev, int eb, DeviceTable &t)
     } else {
         std::memcpy(host.data(), lut->entries.data(), bytes);
     }
+    // The first call on a device may come inside a CUDA graph capture: allocate
+    // and copy in relaxed capture mode on a private non-blocking stream (never
+    // the legacy stream, which would join the capture), so the upload is an
+    // ordinary synchronous host operation that the captured graph does not see.
+    cudaStreamCaptureMode cm = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&cm);
     void *p = nullptr;
+    cudaStream_t us = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess) return set_error(AMSIM_ERR_NOMEM, std::string("cudaMalloc(LUT): ") + cudaGetErrorString(e));
-    e = cudaMemcpy(p, host.data(), bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&us, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p, host.data(), bytes, cudaMemcpyHostToDevice, us);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(us);
+    if (us) cudaStreamDestroy(us);
+    cudaThreadExchangeStreamCaptureMode(&cm);
     if (e != cudaSuccess) {
-        cudaFree(p);
+        if (p) cudaFree(p);
         return set_error(AMSIM_ERR_CUDA, std::string("LUT upload: ") + cudaGetErrorString(e));
     }
     t.ptr = p;
@@ -181,7 +193,7 @@ uint64_t amsim_launch_count(void) { return g_launches.load(); }
 amsim_status amsim_set_path_policy(int policy)
 {
     if (policy < 0 || policy > 63) return set_error(AMSIM_ERR_INVALID_ARG, "policy must be in [0, 63]");
-    g_policy.store(policy);
+    g_policy = policy;
     return AMSIM_OK;
 }
 
@@ -189,7 +201,7 @@ amsim_status amsim_set_multiply_mode(int mode)
 {
     if (mode < AMSIM_MUL_LUT || mode > AMSIM_MUL_DIRECT)
         return set_error(AMSIM_ERR_INVALID_ARG, "multiply mode must be AMSIM_MUL_LUT, _NATIVE or _DIRECT");
-    g_mul_mode.store(mode);
+    g_mul_mode = mode;
     return AMSIM_OK;
 }
 

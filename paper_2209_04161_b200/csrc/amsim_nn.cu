@@ -472,7 +472,7 @@ __device__ float block_reduce(float v, bool is_max, float *sh)
 }
 
 __global__ void __launch_bounds__(NT) softmax_xent_k(const float *z, const int32_t *labels, int N, int K,
-                                                     float *dz, float *row_loss)
+                                                     float inv_n, float *dz, float *row_loss)
 {
     __shared__ float sh[NT / 32];
     const int n = blockIdx.x;
@@ -484,7 +484,6 @@ __global__ void __launch_bounds__(NT) softmax_xent_k(const float *z, const int32
     for (int k = threadIdx.x; k < K; k += NT) s += __expf(zr[k] - m);
     s = block_reduce(s, false, sh);
     const int lab = labels[n];
-    const float inv_n = 1.f / float(N);
     for (int k = threadIdx.x; k < K; k += NT) {
         float p = __expf(zr[k] - m) / s;
         dz[int64_t(n) * K + k] = (p - (k == lab ? 1.f : 0.f)) * inv_n;
@@ -732,17 +731,20 @@ amsim_status amsim_avgpool_bwd(const float *dy, int32_t N, int32_t HW, int32_t C
     return check_launch("amsim_avgpool_bwd");
 }
 
-amsim_status amsim_softmax_xent(const float *logits, const int32_t *labels, int32_t N, int32_t K, float *loss,
-                                float *dlogits, void *ws, size_t ws_bytes, amsim_stream_t stream)
+amsim_status amsim_softmax_xent(const float *logits, const int32_t *labels, int32_t N, int32_t K,
+                                int32_t grad_denominator, float *loss, float *dlogits, void *ws, size_t ws_bytes,
+                                amsim_stream_t stream)
 {
     clear_error();
     if (N <= 0 || K <= 0) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_softmax_xent: N > 0 and K > 0 required");
+    if (grad_denominator < 0) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_softmax_xent: grad_denominator < 0");
     if (!logits || !labels || !loss || !dlogits) return set_error(AMSIM_ERR_INVALID_ARG, "amsim_softmax_xent: null tensor");
     if (!ws || ws_bytes < ws_need(N, 1))
         return set_error(AMSIM_ERR_INVALID_ARG, "amsim_softmax_xent: workspace too small");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     float *row_loss = static_cast<float *>(ws);
-    softmax_xent_k<<<N, NT, 0, st>>>(logits, labels, N, K, dlogits, row_loss);
+    softmax_xent_k<<<N, NT, 0, st>>>(logits, labels, N, K, 1.f / float(grad_denominator ? grad_denominator : N),
+                                     dlogits, row_loss);
     mean_k<<<1, 32, 0, st>>>(row_loss, N, loss);
     count_launch(2);
     return check_launch("amsim_softmax_xent");

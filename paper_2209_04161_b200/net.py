@@ -17,8 +17,10 @@ equal the bench's.  Activations NHWC, weights HWIO, dense weights [in][out].
 Python here only sequences library calls (argument marshalling); the step can
 be captured into one CUDA graph (single GPU).  With several processes the
 weight gradients (conv, dense, BN and bias parameters, one flat buffer) are
-all-reduced in buckets as they become ready (dp.GradAllReducer) and the update
-uses their mean.
+all-reduced in buckets as they become ready (dp.GradAllReducer); the loss
+gradient is divided by the global batch, so their sum is the global-batch mean
+gradient (uneven shards included).  Batch-norm statistics are per rank, as in
+data-parallel training without synchronised batch norm.
 """
 from __future__ import annotations
 
@@ -149,6 +151,16 @@ class Net:
         self.param_index = {id(p): j for j, p in enumerate(self.params)}
         self.reducer = GradAllReducer(self.flat_g, buckets, group=self.group,
                                       comm_stream=torch.cuda.Stream(device=dev) if dev.type == "cuda" else None)
+        # the loss gradient is divided by the GLOBAL batch (sum of the ranks'
+        # shards), so the all-reduce SUM is the gradient of the global-batch
+        # mean loss -- also with uneven shards -- and the update uses lr as is
+        self.global_batch = self.tensors[0].shape[0]
+        if self.reducer.world > 1:
+            import torch.distributed as dist
+            nb = torch.tensor([self.global_batch], dtype=torch.int64,
+                              device=dev if dist.get_backend(self.group) == "nccl" else "cpu")
+            dist.all_reduce(nb, group=self.group)
+            self.global_batch = int(nb.item())
         # scratch: two gradient temporaries, the per-channel reduction workspace, wgrad split-K workspace
         maxn = max(t.numel for t in self.tensors)
         self.scratch = [torch.empty(maxn, device=dev), torch.empty(maxn, device=dev)]
@@ -209,8 +221,9 @@ class Net:
         self.reducer.finish()
 
     def update(self):
-        world = self.reducer.world
-        L.amsim_sgd_momentum(self.flat_w, self.flat_g, self.flat_v, self.flat_w.numel(), self.lr / world,
+        # flat_g holds the global-batch mean gradient (see finalize), so weight
+        # decay and lr apply unscaled whatever the world size
+        L.amsim_sgd_momentum(self.flat_w, self.flat_g, self.flat_v, self.flat_w.numel(), self.lr,
                              self.momentum, self.weight_decay)
 
     def train_step(self):
@@ -421,7 +434,7 @@ class _Loss(_Node):
         if train:   # fused loss + gradient; the backward pass starts from logits.grad
             N, K = self.logits.shape
             L.amsim_softmax_xent(self.logits.data, self.net.labels, N, K, self.net.loss_value, self.logits.grad,
-                                 self.net.nn_ws)
+                                 self.net.nn_ws, grad_denominator=self.net.global_batch)
 
     def bwd(self):
         self.logits.written = True
