@@ -210,7 +210,7 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # BASELINE.json config 5 at N GPUs: one M = N = K approx GEMM, rows sharded
 
-def run_gemm(args, world, rank, gpu, dev):
+def run_gemm(args, world, rank, gpu, dev, comm=None):
     """rows of A / C partitioned over the ranks, B and the
     table replicated (B broadcast from rank 0 outside the timed region), no
     collective on the data path; the all-gather of C is timed separately.
@@ -332,6 +332,7 @@ def run_gemm(args, world, rank, gpu, dev):
                        "l2": f"inputs larger than L2 (B = {4 * n * n / 1e6:.0f} MB)" if 4 * n * n > 126e6
                        else "operands fit the 126 MB L2; not flushed"},
             "clocks": clk,
+            "comm": comm,
             "e2e": e2e,
             "gpu_launches": launches,
             "allgather_ms": gather_ms,
@@ -344,6 +345,46 @@ def run_gemm(args, world, rank, gpu, dev):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+
+
+def relaunch(n: int, backend: str):
+    """`python bench.py --gpus N` without torchrun: re-exec this command under
+    torch.distributed.run with N processes (one per GPU) on 127.0.0.1."""
+    import socket
+
+    import torch
+    if backend == "nccl" and torch.cuda.device_count() < n:
+        raise SystemExit(f"bench.py: --gpus {n} with NCCL needs {n} visible GPUs, found {torch.cuda.device_count()}")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] relaunching as {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
+
+
+def communicator_check(dist, world: int, rank: int, gpu: int, backend: str):
+    """Force communicator creation with one collective, log it, and gather
+    every rank's device (rank 0 reports them in the JSON line)."""
+    import torch
+    t0 = time.perf_counter()
+    t = torch.ones(1, device=torch.device("cuda", gpu) if backend == "nccl" else "cpu")
+    dist.all_reduce(t)
+    if int(t.item()) != world:
+        raise SystemExit(f"bench.py: all-reduce over the communicator gave {int(t.item())}, expected {world}")
+    props = torch.cuda.get_device_properties(gpu)
+    me = {"rank": rank, "gpu": gpu, "uuid": str(getattr(props, "uuid", "")), "host": os.uname().nodename}
+    everyone = [None] * world
+    dist.all_gather_object(everyone, me)
+    ms = (time.perf_counter() - t0) * 1e3
+    print(f"[bench] rank {rank}/{world}: {backend} communicator initialised (nranks={world}, cuda:{gpu}, "
+          f"{ms:.0f} ms)", file=sys.stderr, flush=True)
+    if backend == "nccl" and len({e["uuid"] for e in everyone}) != world:
+        raise SystemExit("bench.py: NCCL ranks share a GPU; one rank per GPU is required")
+    return {"backend": backend, "nranks": dist.get_world_size(), "init_ms": ms,
+            "devices": [(e["rank"], e["gpu"], e["uuid"]) for e in everyone]}
 
 
 def main():
@@ -371,6 +412,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
     if args.impl == "reference":
         run_reference(args)
         return
@@ -378,20 +421,32 @@ def main():
     import torch
     import torch.distributed as dist
 
+    backend = os.environ.get("AMSIM_DIST_BACKEND", "nccl")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args.gpus, backend)           # one process per GPU; does not return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
+    ndev = torch.cuda.device_count()
+    comm = None
     if world > 1:
-        # AMSIM_DIST_BACKEND=gloo + ranks sharing GPUs (gpu = local % count) exercise the
-        # multi-rank path on a 1-GPU box; production is NCCL with one rank per GPU
-        backend = os.environ.get("AMSIM_DIST_BACKEND", "nccl")
-        gpu = local % torch.cuda.device_count()
+        # production: NCCL, one rank per GPU.  AMSIM_DIST_BACKEND=gloo lets ranks share
+        # GPUs (gpu = local % count) to exercise the multi-rank path on a 1-GPU box
+        if backend == "nccl" and ndev < world:
+            raise SystemExit(f"bench.py: --gpus {world} with NCCL needs {world} visible GPUs, found {ndev} "
+                             f"(AMSIM_DIST_BACKEND=gloo shares GPUs for functional tests only)")
+        gpu = local % ndev
         torch.cuda.set_device(gpu)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
         else:
             dist.init_process_group(backend)
+        comm = communicator_check(dist, world, rank, gpu, backend)
     else:
+        if ndev < 1:
+            raise SystemExit("bench.py: no CUDA device visible (no CPU fallback)")
         gpu = 0
         torch.cuda.set_device(0)
     dev = torch.device("cuda", gpu)
@@ -401,7 +456,7 @@ def main():
     from paper_2209_04161_b200.train_step import TrainStep
 
     if args.workload == "gemm":
-        run_gemm(args, world, rank, gpu, dev)
+        run_gemm(args, world, rank, gpu, dev, comm)
         if world > 1:
             dist.destroy_process_group()
         return
@@ -590,6 +645,7 @@ def main():
                        "l2": l2_note,
                        "cuda_graph": use_graph},
             "clocks": clk,
+            "comm": comm,
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": {"bound": "alu", "kernel": f"amsim_mm_kernel [{dom_kind}]", "achieved": achieved,

@@ -412,6 +412,41 @@ def test_conv_operand_order_asymmetric(am, orc):
         assert_bits(got, res.c32, which)
 
 
+def test_plan_cache_separates_symmetric_and_asymmetric_tables(am, luts, orc):
+    """the transposed orientation reads LUT^T, so a plan made for a
+    symmetric table (MBM, 16-bit entries) must not be reused for an asymmetric
+    table of the same m and entry width on the same shape.  The MBM call comes
+    first (it plans the transposed orientation for this 64-channel layer),
+    then the asymmetric table, checked against the oracle in both plans."""
+    import struct
+    from paper_2209_04161_b200 import _lib
+
+    @_lib.MUL_FN
+    def asym(a, b):
+        ub = struct.unpack("<I", struct.pack("<f", b))[0] & 0xFFF00000
+        return a * struct.unpack("<f", struct.pack("<I", ub))[0]
+
+    lut_a = am.Lut.build(asym, 7)
+    assert lut_a.info() == luts("mbm").info() == (7, 16)
+    shape = (4, 16, 16, 64, 64, 3, 3, 1, 1)
+    x, w, dy, OH, OW = _conv_tensors(shape, 500)
+    d, od = am.conv_desc(*shape), orc.conv_desc(*shape)
+    for which in ("fwd", "dgrad", "wgrad"):
+        for pol in (0, 2):
+            am.amsim_set_path_policy(pol)
+            try:
+                _run_conv(am, luts("mbm"), d, x, w, dy, which)          # plans (and caches) for the symmetric table
+                got = _run_conv(am, lut_a, d, x, w, dy, which)
+            finally:
+                am.amsim_set_path_policy(0)
+            ref = {"fwd": lambda: orc.conv_fwd(od, x, w, "asym"), "dgrad": lambda: orc.conv_bwd_data(od, dy, w, "asym"),
+                   "wgrad": lambda: orc.conv_bwd_filter(od, x, dy, "asym")}[which]()
+            if pol:
+                assert_bits(got, ref.c32, f"asym {which} after symmetric plan (exact order)")
+            else:
+                assert_tol(got, ref, f"asym {which} after symmetric plan")
+
+
 @pytest.mark.parametrize("model", ["mbm", "exact"])
 def test_lenet5_step_layers(am, luts, orc, model):
     """BASELINE config 2 shapes (LeNet-5, batch 64) with MNIST-like inputs."""
@@ -514,9 +549,11 @@ def test_dp_shard_sum_equals_full_batch(am, luts, orc):
     assert np.all(np.abs(acc - res.c64) <= 1e-5 * res.abs64 + FLT_MIN)
 
 
-def test_train_step_lenet(am, luts):
-    """The bench's TrainStep on LeNet-5 shapes: every pass through the C ABI;
-    gradients land in the flat all-reduce buffer at the planned offsets."""
+def test_train_step_lenet(am, luts, orc):
+    """The bench's TrainStep on LeNet-5 shapes (default plan, as the bench
+    runs it): every pass through the C ABI; each weight gradient, read from
+    the flat all-reduce buffer at its planned offset, and the outputs of one
+    conv and one dense pass taken from inside the step, against the oracle."""
     import torch
     from paper_2209_04161_b200.train_step import TrainStep
     lut = luts("mbm")
@@ -524,14 +561,151 @@ def test_train_step_lenet(am, luts):
     n0 = am.amsim_launch_count()
     step.step()
     torch.cuda.synchronize()
-    assert am.amsim_launch_count() - n0 >= 13          # 5 fwd + 5 wgrad + 4 dgrad passes
-    assert torch.isfinite(step.flat_grad).all()
-    ly = step.layers[1]                               # c2: compare with a direct ABI call
-    dw = torch.empty_like(ly.dw)
-    ws = torch.empty(max(am.amsim_conv2d_bwd_filter_workspace(lut, ly.desc) // 4, 1), device="cuda")
-    am.amsim_conv2d_bwd_filter(lut, ly.desc, ly.x, ly.dy, dw, ws)
-    torch.cuda.synchronize()
-    assert torch.equal(dw, ly.dw)
+    assert am.amsim_launch_count() - n0 >= 14          # 5 fwd + 5 wgrad + 4 dgrad passes
+    flat = step.flat_grad.cpu().numpy()
+    for ly in step.layers:
+        l = ly.spec
+        x, dy = ly.x.cpu().numpy(), ly.dy.cpu().numpy()
+        off = ly.dw.storage_offset()
+        got = flat[off:off + ly.dw.numel()]
+        if ly.kind == "conv":
+            ref = orc.conv_bwd_filter(orc.conv_desc(l.N, l.H, l.W, l.C, l.K, l.R, l.S, l.stride, l.pad), x, dy, "mbm")
+        else:
+            ref = orc.gemm(np.ascontiguousarray(x.T), dy, "mbm")
+        assert_tol(got.reshape(ref.c64.shape), ref, f"{l.name} wgrad in the flat buffer")
+    # the last forward output of each kind stays in the step's y scratch: re-run
+    # one conv (c2) and one dense (f3) forward pass exactly as forward() does
+    for ly in (step.layers[1], step.layers[2]):
+        l = ly.spec
+        step.timers = None
+        if ly.kind == "conv":
+            y = step.y_scratch[: l.N * l.OH * l.OW * l.K]
+            am.amsim_conv2d_fwd(lut, ly.desc, ly.x, ly.w, y)
+            ref = orc.conv_fwd(orc.conv_desc(l.N, l.H, l.W, l.C, l.K, l.R, l.S, l.stride, l.pad),
+                               ly.x.cpu().numpy(), ly.w.cpu().numpy(), "mbm")
+            assert_tol(host(y).reshape(ref.c64.shape), ref, f"{l.name} fwd")
+        else:
+            y = step.y_scratch[: l.N * l.OUT].view(l.N, l.OUT)
+            am.amsim_gemm(lut, ly.x, ly.w, y)
+            ref = orc.gemm(ly.x.cpu().numpy(), ly.w.cpu().numpy(), "mbm")
+            assert_tol(host(y), ref, f"{l.name} fwd")
+        # dgrad into the dx scratch
+        if ly.kind == "conv":
+            dx = step.dx_scratch[: l.N * l.H * l.W * l.C]
+            am.amsim_conv2d_bwd_data(lut, ly.desc, ly.dy, ly.w, dx)
+            ref = orc.conv_bwd_data(orc.conv_desc(l.N, l.H, l.W, l.C, l.K, l.R, l.S, l.stride, l.pad),
+                                    ly.dy.cpu().numpy(), ly.w.cpu().numpy(), "mbm")
+        else:
+            dx = step.dx_scratch[: l.N * l.IN].view(l.N, l.IN)
+            am.amsim_gemm(lut, ly.dy, ly.w, dx, trans_b=True)
+            ref = orc.gemm(ly.dy.cpu().numpy(), np.ascontiguousarray(ly.w.cpu().numpy().T), "mbm")
+        assert_tol(host(dx).reshape(ref.c64.shape), ref, f"{l.name} dgrad")
+
+
+@pytest.mark.parametrize("model", ["mbm", "exact"])
+def test_lenet5_default_plan(am, luts, orc, model):
+    """BASELINE config 2 (LeNet-5 b64) in the DEFAULT launch plan the bench
+    runs (split-K, transposed orientation, TMA where eligible): tolerance
+    against the oracle for every pass (reading C12)."""
+    lut = luts(model)
+    for i, L in enumerate(inp.lenet5_layers(64)):
+        if isinstance(L, inp.ConvLayer):
+            shape = (L.N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad)
+            x = inp.mnist_like((L.N, L.H, L.W, L.C), 3 + i) if L.first else inp.relu_normal((L.N, L.H, L.W, L.C), 3 + i)
+            w = inp.he_uniform((L.R, L.S, L.C, L.K), L.R * L.S * L.C, 4 + i)
+            dy = inp.normal((L.N, L.OH, L.OW, L.K), 5 + i, 2 ** -8)
+            d, od = am.conv_desc(*shape), orc.conv_desc(*shape)
+            assert_tol(_run_conv(am, lut, d, x, w, dy, "fwd"), orc.conv_fwd(od, x, w, model), L.name + " fwd")
+            assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), orc.conv_bwd_filter(od, x, dy, model), L.name + " wgrad")
+            if not L.first:
+                assert_tol(_run_conv(am, lut, d, x, w, dy, "dgrad"), orc.conv_bwd_data(od, dy, w, model),
+                           L.name + " dgrad")
+        else:
+            X = inp.relu_normal((L.N, L.IN), 3 + i)
+            W = inp.he_uniform((L.IN, L.OUT), L.IN, 4 + i)
+            dY = inp.normal((L.N, L.OUT), 5 + i, 2 ** -8)
+            assert_tol(run_gemm(am, lut, X, W), orc.gemm(X, W, model), L.name + " fwd")
+            assert_tol(run_gemm(am, lut, X, dY, trans_a=True), orc.gemm(X.T.copy(), dY, model), L.name + " wgrad")
+            assert_tol(run_gemm(am, lut, dY, W, trans_b=True), orc.gemm(dY, W.T.copy(), model), L.name + " dgrad")
+
+
+def _distinct(layers):
+    seen, out = set(), []
+    for L in layers:
+        key = (L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, L.first) if isinstance(L, inp.ConvLayer) else \
+            ("dense", L.IN, L.OUT)
+        if key not in seen:
+            seen.add(key)
+            out.append(L)
+    return out
+
+
+R18 = _distinct(inp.resnet18_cifar_layers(128))
+
+
+@pytest.mark.parametrize("name", [L.name for L in R18])
+def test_resnet18_cifar_full_size_sampled(am, luts, orc, name):
+    """BASELINE config 3 (ResNet-18 CIFAR b128): every
+    distinct pass shape at full size with the MBM table.  Default plan:
+    sampled output rows within the reading-C12 tolerance; exact order (no
+    split): the same rows bit-identical to the oracle's c32."""
+    import torch
+    L = {l.name: l for l in R18}[name]
+    g = inp.rng(11)
+    lut = luts("mbm")
+    if isinstance(L, inp.DenseLayer):
+        X = inp.relu_normal((L.N, L.IN), 2000)
+        W = inp.he_normal((L.IN, L.OUT), L.IN, 2001)
+        dY = inp.normal((L.N, L.OUT), 2002, 2 ** -10)
+        for what, A, B, ta, tb in (("fwd", X, W, False, False), ("wgrad", X, dY, True, False),
+                                   ("dgrad", dY, W, False, True)):
+            ref = orc.gemm(A.T.copy() if ta else A, B.T.copy() if tb else B, "mbm")
+            assert_tol(run_gemm(am, lut, A, B, trans_a=ta, trans_b=tb), ref, f"fc {what}")
+            with exact_order(am):
+                assert_bits(run_gemm(am, lut, A, B, trans_a=ta, trans_b=tb), ref.c32, f"fc {what} (exact order)")
+        return
+    shape = (L.N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad)
+    d, od = am.conv_desc(*shape), orc.conv_desc(*shape)
+    x = inp.relu_normal((L.N, L.H, L.W, L.C), 2000)
+    w = inp.he_normal((L.R, L.S, L.C, L.K), L.R * L.S * L.C, 2001)
+    dy = inp.normal((L.N, L.OH, L.OW, L.K), 2002, 2 ** -10)
+    passes = [("fwd", lambda rows: orc.conv_fwd(od, x, w, "mbm", rows=rows), 24),
+              ("wgrad", lambda rows: orc.conv_bwd_filter(od, x, dy, "mbm", rows=rows), 6)]
+    if not L.first:
+        passes.append(("dgrad", lambda rows: orc.conv_bwd_data(od, dy, w, "mbm", rows=rows), 24))
+    for which, oracle_rows, nsamp in passes:
+        out = _run_conv(am, lut, d, x, w, dy, which)
+        rows = np.unique(np.concatenate([[0, out.shape[0] - 1], g.integers(0, out.shape[0], nsamp)]))
+        res = oracle_rows(rows)
+        assert_tol(out[rows], res, f"{name} {which}")
+        with exact_order(am):
+            out = _run_conv(am, lut, d, x, w, dy, which)
+        assert_bits(out[rows], res.c32, f"{name} {which} (exact order)")
+    torch.cuda.empty_cache()
+
+
+def test_resnet50_fc_full_size(am, luts, orc):
+    """The ResNet-50 fc layer at size (256 x 2048 x 1000):
+    fwd Y = X W, wgrad dW = X^T dY, dgrad dX = dY W^T through amsim_gemm in the
+    bench's plan; sampled output rows against the oracle (tolerance), and bit
+    equality with c32 in exact order."""
+    L = [l for l in inp.resnet50_layers(256) if l.name == "fc"][0]
+    g = inp.rng(12)
+    X = inp.relu_normal((L.N, L.IN), 3000)
+    W = inp.he_normal((L.IN, L.OUT), L.IN, 3001)
+    dY = inp.normal((L.N, L.OUT), 3002, 2 ** -10)
+    lut = luts("mbm")
+    for what, A, B, ta, tb in (("fwd", X, W, False, False), ("wgrad", X, dY, True, False),
+                               ("dgrad", dY, W, False, True)):
+        Ao = np.ascontiguousarray(A.T) if ta else A
+        Bo = np.ascontiguousarray(B.T) if tb else B
+        out = run_gemm(am, lut, A, B, trans_a=ta, trans_b=tb)
+        rows = np.unique(np.concatenate([[0, out.shape[0] - 1], g.integers(0, out.shape[0], 30)]))
+        res = orc.gemm(Ao, Bo, "mbm", rows=rows)
+        assert_tol(out[rows], res, f"fc {what}")
+        with exact_order(am):
+            out = run_gemm(am, lut, A, B, trans_a=ta, trans_b=tb)
+        assert_bits(out[rows], res.c32, f"fc {what} (exact order)")
 
 
 # ---------------------------------------------------------------------------
@@ -934,3 +1108,54 @@ def test_gemm_16384_rank_block_sampled(am, luts, orc):
     assert torch.isnan(C[:r0]).all()
     del A, B, C
     torch.cuda.empty_cache()
+
+
+def test_first_call_inside_graph_capture(am, orc):
+    """A table's first use on a device may happen inside CUDA graph capture:
+    the upload runs on a private stream in relaxed capture mode, the graph
+    holds only the compute launch, and its replays give the oracle's bits."""
+    import torch
+    lut = am.Lut.build("mitchell", 6)          # fresh handle: not yet uploaded
+    A = inp.normal((70, 48), 81)
+    B = inp.normal((48, 90), 82)
+    Ad, Bd = dev(A), dev(B)
+    C = torch.full((70, 90), float("nan"), device="cuda")
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    am.amsim_set_path_policy(2)
+    try:
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                am.amsim_gemm(lut, Ad, Bd, C)
+    finally:
+        am.amsim_set_path_policy(0)
+    g.replay()
+    assert_bits(host(C), orc.gemm(A, B, "mitchell", 6).c32, "captured first call")
+    C.fill_(float("nan"))
+    g.replay()
+    assert_bits(host(C), orc.gemm(A, B, "mitchell", 6).c32, "second replay")
+
+
+def test_path_policy_is_per_thread(am, luts, orc):
+    """amsim_set_path_policy affects only the calling thread: a worker thread
+    forcing exact order (policy bit 1) gets the oracle's c32 bits, and the main
+    thread's default-plan result is unchanged before and after."""
+    import threading
+    A = inp.normal((64, 65536), 83)
+    B = inp.normal((65536, 64), 84)
+    lut = luts("mbm")
+    before = run_gemm(am, lut, A, B)
+    out = {}
+
+    def worker():
+        am.amsim_set_path_policy(2)
+        out["exact"] = run_gemm(am, lut, A, B)
+
+    t = threading.Thread(target=worker)
+    t.start()
+    t.join()
+    after = run_gemm(am, lut, A, B)
+    assert_bits(after, before, "main thread default plan")
+    ref = orc.gemm(A, B, "mbm")
+    assert_bits(out["exact"], ref.c32, "worker thread exact order")
+    assert_tol(before, ref, "main thread")
