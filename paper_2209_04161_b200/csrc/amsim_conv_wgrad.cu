@@ -16,7 +16,6 @@ static amsim_status wgrad_plan(const amsim_lut *lut, const amsim_conv2d_desc *d,
     pr.N = d->K;
     pr.M[0] = d->R * d->S * d->C;
     pr.K[0] = d->N * g.OH * g.OW;
-    pr.max_splits = 1024;
     return prepare(lut, p, pr, eb, mode, policy);
 }
 

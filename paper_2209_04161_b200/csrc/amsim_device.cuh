@@ -214,13 +214,21 @@ struct FastDiv {
 
 // ---------------------------------------------------------------------------
 // Problem description: up to MAX_SUB independent sub-GEMMs sharing N (the
-// stride phases of dgrad), each optionally split along K (wgrad).
+// stride phases of dgrad).  Tiles are numbered sub by sub (tile_begin), n
+// fastest.  Schedule (amsim_mm_kernel): tiles [0, n_dp) round-robin over the
+// grid whole ("data-parallel"), tiles [n_dp, ntiles) by STREAM-K -- their
+// k-tiles laid end to end (a tile with K = 0 counts as one position) and cut
+// into sk_G equal contiguous ranges, CTA c taking [c W / sk_G, (c+1) W / sk_G).
+// A tile cut by a range boundary is computed in pieces whose FP32 partial sums
+// are added in increasing k order by the piece that finishes last.
 
 struct SubP {
     int M, K;             // rows and reduction length of this sub-problem
-    int tiles_m, splits, kchunk;
+    int tiles_m;
+    int kt;               // k-tiles per tile (0 when K = 0)
     int tile_begin;       // first global tile index
-    int64_t ws_offset;    // element offset of this sub's split partials [splits][M][N] in the workspace
+    int sk_tile;          // first stream-K tile of this sub (>= tile_begin; tile_end if none)
+    int sk_pos;           // stream-K position of tile sk_tile
 };
 
 struct OpDesc {
@@ -240,9 +248,12 @@ struct KParams {
     int tma_on[2];
     int N, tiles_n, nsub, ntiles;
     SubP sub[MAX_SUB];
+    int n_dp;             // tiles [0, n_dp) data-parallel (round-robin), the rest stream-K
+    int sk_G, sk_W;       // stream-K: CTAs taking part, total positions (k-tiles)
+    int grid;             // CTAs launched
     float *C;             // output (ldc-strided rows, A map's out_row)
-    float *ws;            // split-K partials (subs with splits > 1)
-    int64_t ws_elems;     // workspace size in floats (0: no split)
+    float *ws;            // stream-K partial tiles [2 sk_G][TM * TN][NT], then uint32 counters [ntiles - n_dp]
+    int64_t ws_elems;     // workspace size in 4-byte words (0: no stream-K)
     int cfg;              // host-side tile configuration id
     int64_t ldc;
     int accumulate;
@@ -512,7 +523,7 @@ struct KCfg {
     {
         size_t lut = (lut_bytes + 127) & ~size_t(127);
         return lut + sizeof(float) * RAW_STAGE * STAGES + sizeof(uint32_t) * DEC * 2 + sizeof(uint32_t) * NWARPS * 2 +
-               8 * STAGES + 128;
+               8 * STAGES + 16 + 128;
     }
 };
 
@@ -677,6 +688,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     uint32_t *dec = reinterpret_cast<uint32_t *>(raw + Cf::RAW_STAGE * STAGES);
     uint32_t *wflags = dec + Cf::DEC * 2;  // [2][NWARPS]
     uint64_t *bars = reinterpret_cast<uint64_t *>(wflags + NWARPS * 2);
+    volatile int *sk_last = reinterpret_cast<volatile int *>(bars + STAGES);   // stream-K: this CTA adds the last piece
 
     // table -> shared memory, once per persistent CTA
     if constexpr (!GL && MUL == MUL_LUT) {
@@ -707,39 +719,107 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     const uint32_t elo = uint32_t(p.ecast_lo), ehi = uint32_t(p.ecast_hi);
     const float *dummy = reinterpret_cast<const float *>(p.lut);  // valid global address for 0-byte copies
 
-    struct Tile {
-        int s, m0, n0, kb, ke, split;
+    // Work units: (tile t, k-tile range [k0, k1)); see SubP for the schedule.
+    struct Unit {
+        int t, k0, k1, P;   // P: stream-K position of tile t (stream-K units only)
+        bool sk;
     };
-    auto tile_of = [&](int t) {
-        Tile T;
+    struct Sched {
+        Unit u;             // u.t < 0: no more work
+        int lo, hi;         // this CTA's stream-K position range
+    };
+    auto sub_of = [&](int t) {
         int s = 0;
         while (s + 1 < p.nsub && t >= p.sub[s + 1].tile_begin) s++;
+        return s;
+    };
+    // stream-K position -> unit (first unit of the CTA's range)
+    auto sk_begin = [&](Sched &S) {
+        S.u.t = -1;
+        S.u.sk = true;
+        if (int(blockIdx.x) >= p.sk_G) return;
+        S.lo = int(int64_t(blockIdx.x) * p.sk_W / p.sk_G);
+        S.hi = int(int64_t(blockIdx.x + 1) * p.sk_W / p.sk_G);
+        if (S.lo >= S.hi) return;
+        for (int s = 0; s < p.nsub; s++) {
+            const SubP &B = p.sub[s];
+            const int w = max(B.kt, 1);
+            const int tend = s + 1 < p.nsub ? p.sub[s + 1].tile_begin : p.ntiles;
+            if (B.sk_tile < tend && S.lo < B.sk_pos + (tend - B.sk_tile) * w) {
+                const int i = (S.lo - B.sk_pos) / w;
+                S.u.t = B.sk_tile + i;
+                S.u.P = B.sk_pos + i * w;
+                S.u.k0 = min(S.lo - S.u.P, B.kt);
+                S.u.k1 = min(min(S.hi - S.u.P, w), B.kt);
+                return;
+            }
+        }
+    };
+    auto sched_start = [&](Sched &S) {
+        if (int(blockIdx.x) < p.n_dp) {
+            S.u.t = blockIdx.x;
+            S.u.k0 = 0;
+            S.u.k1 = p.sub[sub_of(S.u.t)].kt;
+            S.u.sk = false;
+        } else {
+            sk_begin(S);
+        }
+    };
+    auto sched_next = [&](Sched &S) {
+        if (!S.u.sk) {
+            const int t = S.u.t + int(gridDim.x);
+            if (t < p.n_dp) {
+                S.u.t = t;
+                S.u.k1 = p.sub[sub_of(t)].kt;
+            } else {
+                sk_begin(S);
+            }
+            return;
+        }
+        const int P = S.u.P + max(p.sub[sub_of(S.u.t)].kt, 1);
+        if (P >= S.hi) {
+            S.u.t = -1;
+            return;
+        }
+        S.u.t++;
+        S.u.P = P;
+        const int kt = p.sub[sub_of(S.u.t)].kt;
+        S.u.k0 = 0;
+        S.u.k1 = min(min(S.hi - P, max(kt, 1)), kt);
+    };
+
+    struct Tile {
+        int s, m0, n0, kb, ke;
+        bool partial;     // a stream-K piece of the tile (partial sums, fixed-order fix-up)
+    };
+    auto tile_of = [&](const Unit &u) {
+        Tile T;
+        const int s = sub_of(u.t);
         const SubP &S = p.sub[s];
-        int local = t - S.tile_begin;
-        int tn = local % p.tiles_n;
-        int r = local / p.tiles_n;
-        int tm = r % S.tiles_m;
-        T.split = r / S.tiles_m;
+        const int local = u.t - S.tile_begin;
         T.s = s;
-        T.m0 = tm * BM;
-        T.n0 = tn * BN;
-        T.kb = T.split * S.kchunk;
-        T.ke = min(S.K, T.kb + S.kchunk);
+        T.m0 = (local / p.tiles_n) * BM;
+        T.n0 = (local % p.tiles_n) * BN;
+        T.kb = u.k0 * BK;
+        T.ke = min(S.K, u.k1 * BK);
+        T.partial = u.sk && (u.k0 > 0 || u.k1 < S.kt);
         return T;
     };
     auto ktiles_of = [&](const Tile &T) { return T.ke > T.kb ? (T.ke - T.kb + BK - 1) / BK : 0; };
 
     // issue cursor (runs STAGES-1 k-tiles ahead of the compute cursor)
-    int itile = blockIdx.x, ik = 0, ig = 0;
+    int ik = 0, ig = 0;
+    Sched IS;
+    sched_start(IS);
     Tile IT;
-    if (itile < p.ntiles) IT = tile_of(itile);
+    if (IS.u.t >= 0) IT = tile_of(IS.u);
     auto issue_next = [&]() {
-        while (itile < p.ntiles) {
+        while (IS.u.t >= 0) {
             int kt = ktiles_of(IT);
             if (ik >= kt) {  // empty k range
-                itile += gridDim.x;
+                sched_next(IS);
                 ik = 0;
-                if (itile < p.ntiles) IT = tile_of(itile);
+                if (IS.u.t >= 0) IT = tile_of(IS.u);
                 continue;
             }
             int stage = ig % STAGES;
@@ -785,8 +865,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             ig++;
             if (++ik == kt) {
                 ik = 0;
-                itile += gridDim.x;
-                if (itile < p.ntiles) IT = tile_of(itile);
+                sched_next(IS);
+                if (IS.u.t >= 0) IT = tile_of(IS.u);
             }
             return;
         }
@@ -798,8 +878,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 #pragma unroll
     for (int c = 0; c < TN; c++) ecur[c] = 0;
     int g = 0;
-    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-        const Tile T = tile_of(tile);
+    Sched CS;
+    sched_start(CS);
+    for (; CS.u.t >= 0; sched_next(CS)) {
+        const Tile T = tile_of(CS.u);
         const int KT = ktiles_of(T);
 #pragma unroll
         for (int r = 0; r < TM; r++)
@@ -970,68 +1052,80 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             }
         }
 
-        // epilogue: this thread's TM x TN outputs (split partials go to the workspace)
         const SubP &S = p.sub[T.s];
-        const bool split_out = S.splits > 1;
-        float *Cb = split_out ? p.ws + S.ws_offset + int64_t(T.split) * S.M * p.N : p.C;
-        if constexpr (TRN) {
-            if (!split_out) {
-                const int row0 = T.m0 + Cf::wrow(warp);
+        if (T.partial) {
+            // Stream-K piece: store the partial sums (slot 2c for the CTA's first
+            // stream-K unit, 2c + 1 for its last; [TM * TN][NT] so every store
+            // and load is coalesced -- thread tid owns the same outputs of the
+            // tile in every CTA), publish, and let the piece that arrives last
+            // add all pieces in increasing k order (deterministic: the pieces and
+            // their order depend only on the plan) and write the tile.
+            const int P = CS.u.P, w = max(S.kt, 1);
+            auto cta_of = [&](int pos) { return int((int64_t(pos + 1) * p.sk_G - 1) / p.sk_W); };
+            auto lo_of = [&](int c) { return int(int64_t(c) * p.sk_W / p.sk_G); };
+            auto slot = [&](int c) {
+                return p.ws + (size_t(2 * c + (lo_of(c) < P ? 1 : 0)) * (TM * TN)) * NT + tid;
+            };
+            const int ca = cta_of(P), cb = cta_of(P + w - 1);
+            float *mine = slot(blockIdx.x);
 #pragma unroll
-                for (int c = 0; c < TN; c++) {
-                    int col = T.n0 + Cf::wcol(warp) + lane * CG + Cf::col(c);
-                    if (col >= p.N) continue;
-                    float *dst = p.C + opb.out_row(T.s, col, p.ldc) + row0;
-                    if (row0 + TM <= S.M && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && !p.accumulate) {
+            for (int r = 0; r < TM; r++)
 #pragma unroll
-                        for (int r = 0; r < TM; r += 4)
-                            *reinterpret_cast<float4 *>(dst + r) =
-                                make_float4(acc[r][c], acc[r + 1][c], acc[r + 2][c], acc[r + 3][c]);
-                    } else {
+                for (int c = 0; c < TN; c++) __stcg(mine + (r * TN + c) * NT, acc[r][c]);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                unsigned *cnt = reinterpret_cast<unsigned *>(p.ws + size_t(2 * p.sk_G) * (TM * TN) * NT);
+                *sk_last = atomicAdd(cnt + (CS.u.t - p.n_dp), 1u) + 1 == unsigned(cb - ca + 1);
+            }
+            __syncthreads();
+            if (!*sk_last) continue;
+            __threadfence();
 #pragma unroll
-                        for (int r = 0; r < TM; r++)
-                            if (row0 + r < S.M) dst[r] = p.accumulate ? dst[r] + acc[r][c] : acc[r][c];
-                    }
-                }
-                continue;
+            for (int r = 0; r < TM; r++)
+#pragma unroll
+                for (int c = 0; c < TN; c++) acc[r][c] = 0.0f;
+            for (int q = ca; q <= cb; q++) {
+                const float *src = slot(q);
+#pragma unroll
+                for (int r = 0; r < TM; r++)
+#pragma unroll
+                    for (int c = 0; c < TN; c++) acc[r][c] += __ldcg(src + (r * TN + c) * NT);
             }
         }
-#pragma unroll
-        for (int r = 0; r < TM; r++) {
-            int row = T.m0 + Cf::wrow(warp) + r;
-            if (row >= S.M) continue;
-            int64_t off;
-            if constexpr (TRN)
-                off = int64_t(row) * p.N;   // only split partials reach here in the transposed orientation
-            else
-                off = split_out ? int64_t(row) * p.N : opa.out_row(T.s, row, p.ldc);
-            float *dst = Cb + off;
+        // epilogue: this thread's TM x TN outputs
+        if constexpr (TRN) {
+            const int row0 = T.m0 + Cf::wrow(warp);
 #pragma unroll
             for (int c = 0; c < TN; c++) {
                 int col = T.n0 + Cf::wcol(warp) + lane * CG + Cf::col(c);
                 if (col >= p.N) continue;
-                dst[col] = (p.accumulate && !split_out) ? (dst[col] + acc[r][c]) : acc[r][c];
+                float *dst = p.C + opb.out_row(T.s, col, p.ldc) + row0;
+                if (row0 + TM <= S.M && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && !p.accumulate) {
+#pragma unroll
+                    for (int r = 0; r < TM; r += 4)
+                        *reinterpret_cast<float4 *>(dst + r) =
+                            make_float4(acc[r][c], acc[r + 1][c], acc[r + 2][c], acc[r + 3][c]);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < TM; r++)
+                        if (row0 + r < S.M) dst[r] = p.accumulate ? dst[r] + acc[r][c] : acc[r][c];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < TM; r++) {
+                int row = T.m0 + Cf::wrow(warp) + r;
+                if (row >= S.M) continue;
+                float *dst = p.C + opa.out_row(T.s, row, p.ldc);
+#pragma unroll
+                for (int c = 0; c < TN; c++) {
+                    int col = T.n0 + Cf::wcol(warp) + lane * CG + Cf::col(c);
+                    if (col >= p.N) continue;
+                    dst[col] = p.accumulate ? (dst[col] + acc[r][c]) : acc[r][c];
+                }
             }
         }
-    }
-}
-
-// Deterministic split-K reduction for sub-problem blockIdx.y:
-// C[out_row(s, i)][j] (+)= sum over splits, in increasing split order
-// (TRN: C[out_row(s, j)][i], opa being the original A operand's map).
-template <class OpA, bool TRN = false>
-__global__ void splitk_reduce_kernel(const __grid_constant__ KParams p, const __grid_constant__ OpA opa)
-{
-    const SubP &S = p.sub[blockIdx.y];
-    if (S.splits <= 1) return;
-    const float *ws = p.ws + S.ws_offset;
-    const int64_t total = int64_t(S.M) * p.N;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-        float s = 0.0f;
-        for (int k = 0; k < S.splits; k++) s += ws[int64_t(k) * total + e];
-        int i = int(e / p.N), j = int(e - int64_t(i) * p.N);
-        float *dst = TRN ? p.C + opa.out_row(blockIdx.y, j, p.ldc) + i : p.C + opa.out_row(blockIdx.y, i, p.ldc) + j;
-        *dst = p.accumulate ? (*dst + s) : s;
     }
 }
 

@@ -124,7 +124,6 @@ struct Problem {
     int nsub = 1;
     int M[MAX_SUB] = {0};
     int K[MAX_SUB] = {0};
-    int max_splits = 64;
     // the A operand is a layer input (ReLU activations in a network): in the
     // transposed orientation it is read by the lanes, where its zeros share one
     // table word and cut bank conflicts (measured +7 % on ResNet-50 l2.1.conv1
@@ -151,80 +150,83 @@ static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t
     }
 }
 
-// Tile plan with a small cost model.  CTAs take tiles round-robin
-// (t = blockIdx.x + i*grid), so a CTA's time is the sum of its tiles' k-tile
-// counts plus a per-tile overhead; split-K (same split count for every
-// sub-problem whose K allows it) trades that makespan against writing and
-// re-reading the partial sums.  Deterministic for a given problem and device.
-static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int policy)
+// Tile plan with a small cost model (cost unit: one k-tile of one BM x BN
+// tile on one SM).  Two schedules (see SubP):
+//  * data-parallel: CTAs take whole tiles round-robin (t = blockIdx.x + i*grid);
+//    a CTA's time is the sum of its tiles' k-tiles plus a per-tile overhead;
+//    every output is the FP32 sum from +0 in increasing k (policy bit 1 forces it);
+//  * stream-K: every SM gets the same number of k-tiles (W / G), whatever the
+//    tile count -- no wave quantisation -- at the price of <= 2 partial tiles per
+//    CTA written, re-read and added in a fixed order by the last piece.
+// The cheaper one is taken.  Deterministic for a given problem and device.
+static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int policy, int NT)
 {
     const int G = num_sms();
     p.N = pr.N;
     p.tiles_n = (pr.N + BN - 1) / BN;
     p.nsub = pr.nsub;
-    int Kmax = 0;
-    for (int s = 0; s < pr.nsub; s++) Kmax = std::max(Kmax, pr.K[s]);
-    const int min_chunk = 4 * BK;   // >= 4 k-tiles per split (small problems need the parallelism)
-    const int max_sp = (policy & 2) ? 1 : std::max(1, std::min(pr.max_splits, Kmax / min_chunk));
-    // cost units: one k-tile of one BM x BN tile
     const double tile_overhead = 2.0;
     const double ktile_s = double(BM) * BN * BK / (20.0 * 1.9e9);     // ~20 approx-MAC/clk/SM
-    const double bytes_per_unit = 5.0e12 * ktile_s / G;               // HBM bytes per cost unit, per SM share
-    double best = 1e300;
-    int best_sp = 1;
-    std::vector<double> load(G);
-    for (int sp = 1; sp <= max_sp; sp = sp < 8 ? sp + 1 : sp + sp / 4) {
-        std::fill(load.begin(), load.end(), 0.0);
-        long t = 0;
-        double red_bytes = 0;
-        for (int s = 0; s < pr.nsub; s++) {
-            int tiles_m = (pr.M[s] + BM - 1) / BM;
-            int ssp = (sp > 1 && pr.K[s] >= 2 * min_chunk) ? sp : 1;
-            int kc = ssp > 1 ? ((pr.K[s] + ssp - 1) / ssp + BK - 1) / BK * BK : std::max(pr.K[s], 1);
-            ssp = ssp > 1 ? (pr.K[s] + kc - 1) / kc : 1;
-            if (ssp > 1) red_bytes += double(ssp + 1) * 4.0 * pr.M[s] * pr.N;
-            for (int sj = 0; sj < ssp; sj++) {
-                int kb = sj * kc, ke = std::min(pr.K[s], kb + kc);
-                double cost = tile_overhead + (ke > kb ? (ke - kb + BK - 1) / BK : 0);
-                long n = long(tiles_m) * p.tiles_n;
-                // round-robin: tile index t .. t+n-1 land on CTAs (t mod G) ...
-                long full = n / G, rem = n % G;
-                if (full)
-                    for (int g = 0; g < G; g++) load[g] += cost * full;
-                for (long r = 0; r < rem; r++) load[(t + full * G + r) % G] += cost;
-                t += n;
-            }
-        }
-        double makespan = *std::max_element(load.begin(), load.end());
-        double total = makespan + red_bytes / (bytes_per_unit * G);
-        if (total < best * 0.98) {  // prefer fewer splits unless clearly better
-            best = total;
-            best_sp = sp;
-        }
-    }
+    const double hbm_per_unit = 5.0e12 * ktile_s;                     // HBM bytes per cost unit (whole chip)
+    const double l2_per_unit_sm = 150.0e9 * ktile_s;                  // L2 bytes one SM reads per cost unit
     int begin = 0;
-    int64_t ws = 0;
+    int64_t W = 0;
     for (int s = 0; s < pr.nsub; s++) {
         SubP &S = p.sub[s];
         S.M = pr.M[s];
         S.K = pr.K[s];
         S.tiles_m = (S.M + BM - 1) / BM;
-        S.splits = 1;
-        S.kchunk = std::max(S.K, 1);
-        if (best_sp > 1 && S.K >= 2 * min_chunk) {
-            int kc = ((S.K + best_sp - 1) / best_sp + BK - 1) / BK * BK;
-            S.splits = (S.K + kc - 1) / kc;
-            S.kchunk = kc;
-        }
+        S.kt = S.K > 0 ? (S.K + BK - 1) / BK : 0;
         S.tile_begin = begin;
-        S.ws_offset = ws;
-        if (S.splits > 1) ws += int64_t(S.splits) * S.M * p.N;
-        begin += S.tiles_m * p.tiles_n * S.splits;
+        begin += S.tiles_m * p.tiles_n;
+        W += int64_t(S.tiles_m) * p.tiles_n * std::max(S.kt, 1);
     }
     p.ntiles = begin;
+    // data-parallel makespan: round-robin simulation
+    std::vector<double> load(G, 0.0);
+    for (int s = 0, t = 0; s < pr.nsub; s++) {
+        const double cost = tile_overhead + p.sub[s].kt;
+        const long n = long(p.sub[s].tiles_m) * p.tiles_n;
+        const long full = n / G, rem = n % G;
+        if (full)
+            for (int g = 0; g < G; g++) load[g] += cost * full;
+        for (long r = 0; r < rem; r++) load[(t + full * G + r) % G] += cost;
+        t = int((t + n) % G);
+    }
+    const double dp = *std::max_element(load.begin(), load.end());
+    // stream-K makespan: W / Gsk k-tiles, the per-unit overhead of the tiles a
+    // range touches, partial tiles through HBM, and the last piece's fix-up
+    // reading every piece of its tile
+    const int min_chunk = 4;   // k-tiles per CTA at least (small problems use fewer CTAs)
+    const int Gsk = int(std::max<int64_t>(1, std::min<int64_t>(G, W / min_chunk)));
+    const double per_cta = double(W) / Gsk;
+    const double units = double(p.ntiles) / Gsk + 1.0;
+    double pieces_max = 1.0;
+    for (int s = 0; s < pr.nsub; s++)
+        pieces_max = std::max(pieces_max, std::ceil(std::max(p.sub[s].kt, 1) / per_cta) + 1.0);
+    const double tile_bytes = 4.0 * BM * BN;
+    const double sk = std::ceil(per_cta) + tile_overhead * units + 2.0 * 2.0 * Gsk * tile_bytes / hbm_per_unit +
+                      pieces_max * tile_bytes / l2_per_unit_sm;
+    bool use_sk = sk < dp * 0.98;
+    // AMSIM_SCHED=dp|sk forces a schedule (tests and tuning only; policy bit 1 still wins)
+    if (const char *f = std::getenv("AMSIM_SCHED"); f && *f) use_sk = f[0] == 's';
+    use_sk = use_sk && !(policy & 2) && W < (int64_t(1) << 30);
+    p.n_dp = use_sk ? 0 : p.ntiles;
+    p.sk_G = use_sk ? Gsk : 0;
+    p.sk_W = use_sk ? int(W) : 0;
+    for (int s = 0, pos = 0; s < pr.nsub; s++) {
+        SubP &S = p.sub[s];
+        const int tend = S.tile_begin + S.tiles_m * p.tiles_n;
+        S.sk_tile = std::min(tend, std::max(S.tile_begin, p.n_dp));
+        S.sk_pos = pos;
+        pos += (tend - S.sk_tile) * std::max(S.kt, 1);
+    }
+    p.grid = std::max(p.n_dp > 0 ? std::min(p.n_dp, G) : 0, p.sk_G);
+    // workspace: 2 partial tiles per stream-K CTA, then one counter per stream-K tile
     p.ws = nullptr;
-    p.ws_elems = ws;
-    return best;
+    p.ws_elems = use_sk ? int64_t(2) * Gsk * BM * BN + (p.ntiles - p.n_dp) : 0;
+    (void)NT;
+    return use_sk ? sk : dp;
 }
 
 // Shared-memory wavefronts per warp-wide lookup, including the operand loads
@@ -252,6 +254,43 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
     return lk + 1.0 / TN + 2.0 / TM;
 }
 
+// Measured cost per padded approx-MAC (ns per G) of each tile configuration
+// with a 16-bit shared-memory table (MBM m = 7) under the stream-K schedule,
+// median over the ResNet-50 b256 passes of `tools/cfg_sweep.py`
+// (profiles/r02_cfg_sweep_b256.jsonl): dense operands (dgrad) and layer-input
+// A operands (fwd / wgrad: zero-row skipping in the normal orientation, sparse
+// lanes in the transposed one).  The wavefront model below under-prices the
+// instruction overhead of the smaller register tiles (Big 16x4 measures 1.13x
+// Huge 16x8 per MAC where the wavefronts predict 1.05x).  < 0: not measured.
+static double measured_cost16(CfgId c, bool trn, bool act)
+{
+    if (trn) {
+        switch (c) {
+        case CfgId::Huge: return act ? 0.2583 : 0.2752;
+        case CfgId::Big: return act ? 0.2812 : 0.2990;
+        case CfgId::Flat: return act ? 0.2866 : 0.3159;
+        case CfgId::Flat3: return act ? 0.3112 : 0.3229;
+        case CfgId::TallT: return act ? 0.3122 : 0.3340;
+        case CfgId::Wide: return act ? 0.3240 : 0.3462;
+        default: return -1.0;
+        }
+    }
+    switch (c) {
+    case CfgId::Huge: return act ? 0.2190 : 0.2732;
+    case CfgId::Big: return act ? 0.2649 : 0.3077;
+    case CfgId::Flat: return act ? 0.2705 : 0.3104;
+    case CfgId::Mid: return act ? 0.3487 : 0.3605;
+    case CfgId::Lean: return act ? 0.4236 : 0.4391;
+    case CfgId::Small: return act ? 0.5630 : 0.5970;
+    // offered only for <= 64 (Wide) / 129..160 rows (Tall), absent from the sweep's
+    // shapes: Tall from the r01 stem-wgrad ratio to TallT^T (1.093), Wide between
+    // Big and Wide^T
+    case CfgId::Tall: return act ? 0.3410 : 0.3600;
+    case CfgId::Wide: return act ? 0.3000 : 0.3300;
+    default: return -1.0;
+    }
+}
+
 static int cfg_tn(CfgId c)
 {
     switch (c) {
@@ -267,7 +306,7 @@ static int cfg_tn(CfgId c)
 // Plan cache: the same problem (shape, table width, mode, policy) is planned
 // once per process.
 struct PlanRec {
-    int cfg, tiles_n, nsub, ntiles, trn;
+    int cfg, tiles_n, nsub, ntiles, trn, n_dp, sk_G, sk_W, grid;
     int64_t ws_elems;
     SubP sub[MAX_SUB];
 };
@@ -313,10 +352,12 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     const uint32_t smem_lut = smem_table ? bytes : 0u;
     int force = -1;   // AMSIM_FORCE_CFG: tuning experiments only (>= 10: transposed orientation, cfg - 10)
     if (const char *f = std::getenv("AMSIM_FORCE_CFG"); f && *f) force = std::atoi(f);
+    int sched = 0;     // AMSIM_SCHED (tile_plan): part of the cache key
+    if (const char *f = std::getenv("AMSIM_SCHED"); f && *f) sched = f[0];
     // lut->symmetric decides whether the transposed orientation (which reads
     // LUT^T) may be planned, so it is part of the key
-    std::vector<int64_t> key = {pr.N, pr.nsub, pr.max_splits, pr.a_is_activation, eb, p.lut_global, p.mul, policy & (3 | 16), mbits,
-                                num_sms(), force, lut->symmetric ? 1 : 0};
+    std::vector<int64_t> key = {pr.N, pr.nsub, pr.a_is_activation, eb, p.lut_global, p.mul, policy & (3 | 16), mbits,
+                                num_sms(), force, lut->symmetric ? 1 : 0, sched};
     for (int i = 0; i < pr.nsub; i++) {
         key.push_back(pr.M[i]);
         key.push_back(pr.K[i]);
@@ -327,7 +368,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         if (it != g_plans.end()) {
             const PlanRec &r = it->second;
             p.cfg = r.cfg; p.trn = r.trn; p.N = r.trn ? pr.M[0] : pr.N; p.tiles_n = r.tiles_n; p.nsub = r.nsub;
-            p.ntiles = r.ntiles;
+            p.ntiles = r.ntiles; p.n_dp = r.n_dp; p.sk_G = r.sk_G; p.sk_W = r.sk_W; p.grid = r.grid;
             p.ws_elems = r.ws_elems; p.ws = nullptr;
             std::memcpy(p.sub, r.sub, sizeof(r.sub));
             return AMSIM_OK;
@@ -363,6 +404,11 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     if (force >= 10 && trn_ok) cands.clear();
     double best = 1e300;
     KParams bestp = p;
+    // 16-bit shared-memory tables at m = 7 (MBM / exact): measured per-configuration
+    // costs; otherwise the wavefront model, scaled to the same units (Huge: 2.30
+    // wavefronts per lookup <-> 0.2732)
+    const bool measured16 = smem_table && eb == 16 && mbits == 7 && p.mul == MUL_LUT;
+    const double wf_to_cost16 = 0.2732 / 2.30;
     for (CfgId c : cands) {
         int BM, BN, NT;
         size_t smem;
@@ -371,14 +417,17 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         KParams q = p;
         q.cfg = int(c);
         q.trn = 0;
-        double cost = tile_plan(q, pr, BM, BN, policy) * double(BM) * BN * wf_per_lookup(c, eb, mbits, smem_table);
+        const double m16 = measured16 ? measured_cost16(c, false, pr.a_is_activation) : -1.0;
+        double cost = tile_plan(q, pr, BM, BN, policy, NT) * double(BM) * BN *
+                      (m16 > 0 ? m16 : wf_per_lookup(c, eb, mbits, smem_table) * wf_to_cost16);
         // zero-row skipping (SKIP in amsim_mm_kernel): in this orientation a layer
         // input's zeros (ReLU) are warp-shared rows whose lookups are predicated
         // off.  The saving grows with the columns per lane (the predicate and the
         // operand loads are per row): measured on ResNet-50 (MBM, m = 7) at
         // 0.87-0.89 of Huge^T for Huge (16 x 8), 0.96-1.04 for Big (16 x 4),
-        // none for 2-column tiles -- factors calibrated on those ratios.
-        if (pr.a_is_activation && AMSIM_SKIP && smem_table && eb >= 16 && p.mul == MUL_LUT)
+        // none for 2-column tiles -- factors calibrated on those ratios
+        // (the measured 16-bit costs include it).
+        if (m16 < 0 && pr.a_is_activation && AMSIM_SKIP && smem_table && eb >= 16 && p.mul == MUL_LUT)
             cost *= cfg_tn(c) >= 8 ? 0.84 : cfg_tn(c) >= 4 ? 0.92 : 1.0;
         if (cost < best * 0.999) {
             best = cost;
@@ -410,8 +459,10 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
             KParams q = p;
             q.cfg = int(c);
             q.trn = 1;
-            double cost = tile_plan(q, pt, BM, BN, policy) * double(BM) * BN * wf_per_lookup(c, eb, mbits, smem_table) *
-                          (pr.a_is_activation ? 0.95 : 1.0);
+            const double m16 = measured16 ? measured_cost16(c, true, pr.a_is_activation) : -1.0;
+            double cost = tile_plan(q, pt, BM, BN, policy, NT) * double(BM) * BN *
+                          (m16 > 0 ? m16 : wf_per_lookup(c, eb, mbits, smem_table) * wf_to_cost16 *
+                                               (pr.a_is_activation ? 0.95 : 1.0));
             if (cost < best * 0.999) {
                 best = cost;
                 bestp = q;
@@ -421,11 +472,13 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     if (best >= 1e299) return set_error(AMSIM_ERR_UNSUPPORTED, "no tile configuration fits shared memory");
     p = bestp;
     if (const char *dbg = std::getenv("AMSIM_DEBUG_PLAN"); dbg && *dbg && *dbg != '0')
-        std::fprintf(stderr, "[amsim plan] N=%d M0=%d K0=%d nsub=%d eb=%d mul=%d -> cfg=%d trn=%d tiles=%d splits0=%d ws=%lld\n",
-                     pr.N, pr.M[0], pr.K[0], pr.nsub, eb, p.mul, p.cfg, p.trn, p.ntiles, p.sub[0].splits,
+        std::fprintf(stderr, "[amsim plan] N=%d M0=%d K0=%d nsub=%d eb=%d mul=%d -> cfg=%d trn=%d tiles=%d n_dp=%d "
+                     "sk_G=%d sk_W=%d ws=%lld\n",
+                     pr.N, pr.M[0], pr.K[0], pr.nsub, eb, p.mul, p.cfg, p.trn, p.ntiles, p.n_dp, p.sk_G, p.sk_W,
                      (long long)p.ws_elems);
     PlanRec r;
     r.cfg = p.cfg; r.trn = p.trn; r.tiles_n = p.tiles_n; r.nsub = p.nsub; r.ntiles = p.ntiles; r.ws_elems = p.ws_elems;
+    r.n_dp = p.n_dp; r.sk_G = p.sk_G; r.sk_W = p.sk_W; r.grid = p.grid;
     std::memcpy(r.sub, p.sub, sizeof(r.sub));
     std::lock_guard<std::mutex> g(g_plan_mu);
     if (g_plans.size() >= kPlanCacheMax) g_plans.clear();   // bounded: a process planning many shapes re-plans
@@ -448,7 +501,7 @@ static amsim_status launch_cfg(const KParams &p, const OpA &a, const OpB &b, cud
         if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute");
         opted.fetch_or(1ull << (dev & 63));
     }
-    int grid = std::min(p.ntiles, num_sms());
+    const int grid = p.grid;
     if (grid <= 0) return AMSIM_OK;
     kern<<<grid, Cf::NT, smem, st>>>(p, a, b);
     count_launch();
@@ -714,9 +767,9 @@ static amsim_status launch_trn(const KParams &p, const OpR &r, const OpC &c, cud
     return set_error(AMSIM_ERR_UNSUPPORTED, "internal: transposed orientation with this tile configuration");
 }
 
-// Launch the GEMM core and, when the plan splits K, the fixed-order reduction.
-// `ws` is the caller's workspace (>= p.ws_elems floats) or nullptr, in which
-// case a stream-ordered allocation is used.
+// Launch the GEMM core.  A stream-K plan needs `ws` (partial tiles and tile
+// counters, p.ws_elems words): the caller's workspace or, when nullptr, a
+// stream-ordered allocation; its counters are zeroed on the stream first.
 template <class OpA, class OpB>
 static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStream_t st, float *ws = nullptr)
 {
@@ -730,6 +783,13 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
             own = true;
         }
         p.ws = ws;
+        // stream-K tile counters start at zero (one per stream-K tile, after the partial slots)
+        const int64_t slots = p.ws_elems - (p.ntiles - p.n_dp);
+        cudaError_t e = cudaMemsetAsync(ws + slots, 0, size_t(p.ntiles - p.n_dp) * 4, st);
+        if (e != cudaSuccess) {
+            if (own) scratch_free(ws, st);
+            return cuda_check(e, "stream-K counter reset");
+        }
     }
     int BM, BN, NT;
     size_t smem;
@@ -746,17 +806,6 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
         s = (eb == 8 && p.mul == MUL_LUT)    ? launch_eb<8>(p, a, b, st)
             : (eb == 16 && p.mul == MUL_LUT) ? launch_eb<16>(p, a, b, st)
                                              : launch_eb<32>(p, a, b, st);
-    }
-    if (s == AMSIM_OK && p.ws_elems > 0) {
-        int64_t maxmn = 0;
-        for (int i = 0; i < p.nsub; i++) maxmn = std::max<int64_t>(maxmn, int64_t(p.sub[i].M) * p.N);
-        int bx = int(std::max<int64_t>(1, std::min<int64_t>((maxmn + 255) / 256, 4L * num_sms())));
-        if (p.trn)
-            splitk_reduce_kernel<OpA, true><<<dim3(bx, p.nsub), 256, 0, st>>>(p, a);
-        else
-            splitk_reduce_kernel<OpA><<<dim3(bx, p.nsub), 256, 0, st>>>(p, a);
-        count_launch();
-        s = cuda_check(cudaGetLastError(), "splitk_reduce launch");
     }
     if (own) scratch_free(ws, st);
     return s;

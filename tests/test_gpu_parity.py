@@ -380,8 +380,15 @@ def test_entry_layout_never_changes_bits(am, luts, orc, model, m, width):
         finally:
             am.amsim_set_path_policy(0)
     for i in range(4):
-        assert_bits(outs[0][i], outs[4][i], f"{model} m={m} part {i} split")
+        # default plans compare bit for bit while both layouts keep the table in
+        # shared memory (same tile configuration, hence the same stream-K
+        # pieces); the 32-bit m = 8 table (256 KB) moves to global memory with
+        # its own tile set, so there only the exact order is layout-independent
+        if m <= 7:
+            assert_bits(outs[0][i], outs[4][i], f"{model} m={m} part {i} split")
         assert_bits(outs[2][i], outs[6][i], f"{model} m={m} part {i} exact order")
+    assert_tol(outs[0][3], orc.conv_bwd_filter(orc.conv_desc(*shape), x, dy, model, m), "wgrad default plan")
+    assert_tol(outs[4][3], orc.conv_bwd_filter(orc.conv_desc(*shape), x, dy, model, m), "wgrad default plan, 32-bit")
     assert_bits(outs[2][0], orc.gemm(A, B, model, m).c32, "gemm vs c32")
     assert_bits(outs[2][1], orc.conv_fwd(orc.conv_desc(*shape), x, w, model, m).c32, "fwd vs c32")
 
@@ -736,10 +743,13 @@ def test_direct_mode_conv_equals_table(am, luts, model):
     shape = (2, 14, 14, 16, 72, 3, 3, 2, 1)
     x, w, dy, OH, OW = _conv_tensors(shape, 91)
     d = am.conv_desc(*shape)
+    # exact order: the direct mode plans its own tile shapes (no table in shared
+    # memory), so only the fixed k order makes the two plans comparable bit for bit
     for which in ("fwd", "dgrad", "wgrad"):
-        ref = _run_conv(am, lut, d, x, w, dy, which)
-        with am.multiply_mode(am.AMSIM_MUL_DIRECT):
-            got = _run_conv(am, lut, d, x, w, dy, which)
+        with exact_order(am):
+            ref = _run_conv(am, lut, d, x, w, dy, which)
+            with am.multiply_mode(am.AMSIM_MUL_DIRECT):
+                got = _run_conv(am, lut, d, x, w, dy, which)
         assert_bits(got, ref, f"{model} {which}")
 
 
@@ -1159,3 +1169,70 @@ def test_path_policy_is_per_thread(am, luts, orc):
     ref = orc.gemm(A, B, "mbm")
     assert_bits(out["exact"], ref.c32, "worker thread exact order")
     assert_tol(before, ref, "main thread")
+
+
+# ---------------------------------------------------------------------------
+# stream-K schedule (SubP in csrc/amsim_device.cuh): pieces of a tile summed
+# in increasing k by the last piece to finish
+
+SK_CASES = [
+    # (kind, args): GEMM (M, N, K) or conv shape; chosen so tiles are cut into
+    # 1, 2 and many pieces, with fewer stream-K CTAs than SMs, ragged edges,
+    # several sub-problems with K = 0 tiles (strided 1x1 / stride-3 dgrad)
+    ("gemm", (64, 64, 200000)),        # one tile, cut into ~G pieces
+    ("gemm", (130, 70, 3000)),         # few tiles, W / 4 < G: fewer CTAs
+    ("gemm", (1000, 300, 777)),        # ragged, pieces straddle tile ends
+    ("gemm", (2048, 1000, 256)),       # the ResNet-50 fc shape (tile count not a multiple of G)
+    ("conv", (3, 17, 17, 16, 24, 1, 1, 2, 0)),    # 1x1 stride 2: 3 of 4 dgrad phases have K = 0
+    ("conv", (2, 19, 19, 16, 32, 3, 3, 3, 1)),    # stride 3: 9 phases, uneven K
+    ("conv", (4, 16, 16, 64, 64, 3, 3, 1, 1)),    # 64-channel layer (transposed orientation)
+]
+
+
+@pytest.mark.parametrize("case", range(len(SK_CASES)))
+@pytest.mark.parametrize("sched", ["sk", "dp"])
+def test_stream_k_schedule(am, luts, orc, case, sched, monkeypatch):
+    """Forced stream-K (AMSIM_SCHED=sk) and forced data-parallel tiles give
+    results within the reading-C12 tolerance of the oracle, and a repeated
+    call is bit-identical (the pieces and their order depend only on the
+    plan, not on which CTA finishes last)."""
+    monkeypatch.setenv("AMSIM_SCHED", sched)
+    kind, args = SK_CASES[case]
+    lut = luts("mbm")
+    if kind == "gemm":
+        M, N, K = args
+        A = inp.normal((M, K), 90 + case)
+        B = inp.normal((K, N), 91 + case)
+        outs = [run_gemm(am, lut, A, B) for _ in range(2)]
+        assert_bits(outs[1], outs[0], "repeat")
+        rows = np.unique(np.concatenate([[0, M - 1], inp.rng(case).integers(0, M, 20)]))
+        assert_tol(outs[0][rows], orc.gemm(A, B, "mbm", rows=rows), f"gemm {args}")
+        C0 = inp.normal((M, N), 92 + case)
+        got = run_gemm(am, lut, A, B, C0=C0, accumulate=True)
+        ref = orc.gemm(A, B, "mbm", rows=rows)
+        err = np.abs(got[rows].astype(np.float64) - (ref.c64 + C0[rows]))
+        assert np.all(err <= 1e-5 * (ref.abs64 + np.abs(C0[rows])) + FLT_MIN), "accumulate"
+        return
+    x, w, dy, OH, OW = _conv_tensors(args, 95 + case)
+    d, od = am.conv_desc(*args), orc.conv_desc(*args)
+    for which, ref in (("fwd", lambda: orc.conv_fwd(od, x, w, "mbm")), ("dgrad", lambda: orc.conv_bwd_data(od, dy, w, "mbm")),
+                       ("wgrad", lambda: orc.conv_bwd_filter(od, x, dy, "mbm"))):
+        outs = [_run_conv(am, lut, d, x, w, dy, which) for _ in range(2)]
+        assert_bits(outs[1], outs[0], f"{which} repeat")
+        assert_tol(outs[0], ref(), f"{args} {which}")
+
+
+def test_stream_k_transposed_and_forced_configs(am, luts, orc, monkeypatch):
+    """Stream-K pieces in the transposed orientation (the epilogue writes
+    C^T) and with several forced tile configurations."""
+    monkeypatch.setenv("AMSIM_SCHED", "sk")
+    shape = (2, 20, 20, 64, 48, 3, 3, 1, 1)
+    x, w, dy, OH, OW = _conv_tensors(shape, 120)
+    d, od = am.conv_desc(*shape), orc.conv_desc(*shape)
+    lut = luts("mbm")
+    refs = {"fwd": orc.conv_fwd(od, x, w, "mbm"), "dgrad": orc.conv_bwd_data(od, dy, w, "mbm"),
+            "wgrad": orc.conv_bwd_filter(od, x, dy, "mbm")}
+    for force in ("14", "12", "16", "2", "5", "0"):
+        monkeypatch.setenv("AMSIM_FORCE_CFG", force)
+        for which, ref in refs.items():
+            assert_tol(_run_conv(am, lut, d, x, w, dy, which), ref, f"force={force} {which}")

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--model", default="mbm")
     ap.add_argument("--m", type=int, default=7)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the workload's global batch)")
     args = ap.parse_args()
 
     import torch
@@ -37,7 +38,7 @@ def main():
     from amsim_inputs import device as gen
     import paper_2209_04161_b200 as am
 
-    batch = {"resnet50": 256, "resnet18": 128, "lenet5": 64}[args.workload]
+    batch = args.batch or {"resnet50": 256, "resnet18": 128, "lenet5": 64}[args.workload]
     layers = {"resnet50": inp.resnet50_layers, "resnet18": inp.resnet18_cifar_layers,
               "lenet5": inp.lenet5_layers}[args.workload](batch)
     lut = am.Lut.build(args.model, args.m)

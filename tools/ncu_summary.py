@@ -16,6 +16,10 @@ WANT = [
     ("launch__shared_mem_per_block_dynamic", "dyn smem/CTA"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
     ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue active %"),
+    ("sm__cycles_active.avg", "SM active cycles (avg)"),
+    ("sm__cycles_active.max", "SM active cycles (max)"),
+    ("sm__cycles_active.min", "SM active cycles (min)"),
+    ("sm__cycles_elapsed.max", "SM elapsed cycles"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("sass__inst_executed_shared_loads", "shared load instr"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "smem load wavefronts"),
