@@ -126,10 +126,25 @@ def oracle_gemm_sample(n: int, model: str, m: int, budget_s: float):
     return macs, dt, oracle.num_threads(), desc
 
 
-def oracle_sample(workload: str, model: str, m: int, budget_s: float, size: int = 16384):
+def cpu_info():
+    """CPU model name and logical core count of this host (cpu_baseline context)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def oracle_sample(workload: str, model: str, m: int, budget_s: float, size: int = 16384, keep=0):
     """Run the oracle over the workload's layer passes at batch 1 (in step
     order: all forwards, then wgrad/dgrad in reverse) until `budget_s` is
-    spent.  Returns (macs, seconds, threads, description)."""
+    spent.  Returns (macs, seconds, threads, description[, kept]) -- with keep > 0
+    also the inputs and oracle results of the first `keep` passes, for the
+    GPU-vs-oracle check of the same sample (sample_parity)."""
     import numpy as np
 
     import amsim_inputs as inp
@@ -142,6 +157,7 @@ def oracle_sample(workload: str, model: str, m: int, budget_s: float, size: int 
     macs = 0
     t0 = time.perf_counter()
     done = 0
+    kept = []
     for i, (kind, l) in enumerate(passes):
         if isinstance(l, inp.ConvLayer):
             d = oracle.conv_desc(l.N, l.H, l.W, l.C, l.K, l.R, l.S, l.stride, l.pad)
@@ -149,21 +165,23 @@ def oracle_sample(workload: str, model: str, m: int, budget_s: float, size: int 
             w = inp.he_normal((l.R, l.S, l.C, l.K), l.R * l.S * l.C, 11 + i)
             dy = inp.normal((l.N, l.OH, l.OW, l.K), 12 + i, 2 ** -10)
             if kind == "fwd":
-                oracle.conv_fwd(d, x, w, model, m)
+                res = oracle.conv_fwd(d, x, w, model, m)
             elif kind == "wgrad":
-                oracle.conv_bwd_filter(d, x, dy, model, m)
+                res = oracle.conv_bwd_filter(d, x, dy, model, m)
             else:
-                oracle.conv_bwd_data(d, dy, w, model, m)
+                res = oracle.conv_bwd_data(d, dy, w, model, m)
         else:
             x = inp.relu_normal((l.N, l.IN), 10 + i)
             w = inp.he_normal((l.IN, l.OUT), l.IN, 11 + i)
             dy = inp.normal((l.N, l.OUT), 12 + i, 2 ** -10)
             if kind == "fwd":
-                oracle.gemm(x, w, model, m)
+                res = oracle.gemm(x, w, model, m)
             elif kind == "wgrad":
-                oracle.gemm(np.ascontiguousarray(x.T), dy, model, m)
+                res = oracle.gemm(np.ascontiguousarray(x.T), dy, model, m)
             else:
-                oracle.gemm(dy, np.ascontiguousarray(w.T), model, m)
+                res = oracle.gemm(dy, np.ascontiguousarray(w.T), model, m)
+        if len(kept) < keep:
+            kept.append((kind, l, x, w, dy, res))
         macs += l.macs()
         done += 1
         if time.perf_counter() - t0 > budget_s:
@@ -171,7 +189,44 @@ def oracle_sample(workload: str, model: str, m: int, budget_s: float, size: int 
     dt = time.perf_counter() - t0
     desc = (f"{workload} at batch 1: first {done} of {len(passes)} layer passes in step order "
             f"({macs / 1e9:.2f} G approx-MACs), plain-C oracle -O2 OpenMP")
+    if keep:
+        return macs, dt, oracle.num_threads(), desc, kept
     return macs, dt, oracle.num_threads(), desc
+
+
+def sample_parity(am, lut, kept):
+    """The GPU path on the cpu_baseline sample's own inputs: every kept pass
+    through the C ABI, compared with the oracle's result element by element
+    (|gpu - c64| <= 1e-5 sum|p| + FLT_MIN, reading C12).  Returns a summary."""
+    import numpy as np
+    import torch
+    worst, n_el = 0.0, 0
+    for kind, l, x, w, dy, res in kept:
+        X, Wt, DY = (torch.from_numpy(np.ascontiguousarray(t)).cuda() for t in (x, w, dy))
+        if hasattr(l, "H"):
+            d = am.conv_desc(l.N, l.H, l.W, l.C, l.K, l.R, l.S, l.stride, l.pad)
+            if kind == "fwd":
+                out = torch.empty((l.N, l.OH, l.OW, l.K), device="cuda")
+                am.amsim_conv2d_fwd(lut, d, X, Wt, out)
+            elif kind == "wgrad":
+                out = torch.empty((l.R, l.S, l.C, l.K), device="cuda")
+                ws = torch.empty(max(am.amsim_conv2d_bwd_filter_workspace(lut, d) // 4, 1), device="cuda")
+                am.amsim_conv2d_bwd_filter(lut, d, X, DY, out, ws)
+            else:
+                out = torch.empty((l.N, l.H, l.W, l.C), device="cuda")
+                am.amsim_conv2d_bwd_data(lut, d, DY, Wt, out)
+        else:
+            if kind == "fwd":
+                out = am.amsim_gemm(lut, X, Wt, torch.empty((l.N, l.OUT), device="cuda"))
+            elif kind == "wgrad":
+                out = am.amsim_gemm(lut, X, DY, torch.empty((l.IN, l.OUT), device="cuda"), trans_a=True)
+            else:
+                out = am.amsim_gemm(lut, DY, Wt, torch.empty((l.N, l.IN), device="cuda"), trans_b=True)
+        got = out.cpu().numpy().reshape(res.c64.shape).astype(np.float64)
+        tol = 1e-5 * res.abs64 + np.finfo(np.float32).tiny
+        worst = max(worst, float(np.max(np.abs(got - res.c64) / tol)))
+        n_el += got.size
+    return {"passes": len(kept), "elements": n_el, "max_err_over_tol": worst, "ok": worst <= 1.0}
 
 
 def run_reference(args):
@@ -201,7 +256,8 @@ def run_reference(args):
         "data": "synthetic (seeded, shapes and value distributions of the paper's workloads)",
         "config": {"workload": workload_label(args.workload, args.model, args.m, args.size) + " [oracle sample]",
                    "model": args.model, "m": args.m},
-        "cpu_baseline": {"value": value, "unit": "GMAC/s", "cores": threads, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "GMAC/s", "cores": threads, "kind": "oracle", "sample": desc,
+                         **cpu_info()},
         "e2e": {"value": value, "unit": "GMAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -315,7 +371,8 @@ def run_gemm(args, world, rank, gpu, dev, comm=None):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cm, dt, threads, desc = oracle_gemm_sample(n, args.model, args.m, args.cpu_budget)
-            cpu = {"value": cm / dt / 1e9, "unit": "GMAC/s", "cores": threads, "kind": "oracle", "sample": desc}
+            cpu = {"value": cm / dt / 1e9, "unit": "GMAC/s", "cores": threads, "kind": "oracle", "sample": desc,
+                   **cpu_info()}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "GMAC/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {ex}"}
@@ -403,6 +460,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-exact-step", action="store_true",
+                    help="skip timing the same step with the exact bf16 table (reported next to the MBM number)")
     ap.add_argument("--policy", type=int, default=0, help="amsim_set_path_policy bits (A/B experiments only)")
     ap.add_argument("--no-full-step", action="store_true",
                     help="skip the whole-network training / inference step measurement (net.py)")
@@ -541,6 +600,28 @@ def main():
     except Exception as ex:  # noqa: BLE001
         lut_meas = f"unavailable: {ex}"
 
+    # ---- the same step with the exact (bfloat16-by-truncation) table: every
+    # product pinned to the IEEE product of truncated operands,
+    # so this rate has no stand-in model behind it ----
+    exact_step = None
+    zero_frac = step.activation_zero_fraction()
+    if not args.no_exact_step and args.model != "exact" and not use_graph:
+        step.set_lut(am.Lut.build("exact", args.m))
+        for _ in range(2):
+            step.step()
+        barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record()
+        for _ in range(args.steps):
+            step.step()
+        x1.record()
+        barrier()
+        xms = max_over_ranks(x0.elapsed_time(x1) / args.steps, dev)
+        exact_step = {"model": "exact", "m": args.m, "ms_per_step": xms,
+                      "value": total_macs / (xms * 1e-3) / 1e9, "unit": "GMAC/s",
+                      "note": "same step, exact table: products pinned to the IEEE product of bf16-truncated operands"}
+        step.set_lut(lut)
+
     # ---- end to end: pinned host input -> device, step, gradients -> host ----
     e2e = None
     if not args.no_e2e:
@@ -605,22 +686,25 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            macs, dt, threads, desc = oracle_sample(args.workload, args.model, args.m, args.cpu_budget)
-            cpu = {"value": macs / dt / 1e9, "unit": "GMAC/s", "cores": threads, "kind": "oracle", "sample": desc}
+            macs, dt, threads, desc, kept = oracle_sample(args.workload, args.model, args.m, args.cpu_budget, keep=6)
+            cpu = {"value": macs / dt / 1e9, "unit": "GMAC/s", "cores": threads, "kind": "oracle", "sample": desc,
+                   **cpu_info(), "sample_parity": sample_parity(am, lut, kept)}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "GMAC/s", "cores": os.cpu_count(), "kind": "oracle",
-                   "sample": f"failed: {ex}"}
+                   "sample": f"failed: {ex}", **cpu_info()}
 
     # DRAM traffic of the dominant kernel kind per layer pass, from the committed
     # ncu launch list of this same command (profiles/; tools/summarize_launches.py)
     traffic, traffic_note = None, None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if args.workload == "resnet50" and os.path.exists(tpath):
         t = json.load(open(tpath)).get(dom_kind)
         if t:
             traffic = t["dram_bytes_per_pass"]
             traffic_note = (f"ncu dram bytes per {dom_kind} pass (avg over {t['layer_passes']} passes) from "
-                            f"profiles/r01_traffic.json; algorithmic 4(|X|+|W|+|Y|) = "
+                            f"profiles/{os.path.basename(tpath)}; algorithmic 4(|X|+|W|+|Y|) = "
                             f"{t['algorithmic_bytes_per_pass']:.4g} B/pass (ratio {t['ratio']:.3f})")
 
     ws_bytes = 0
@@ -642,6 +726,7 @@ def main():
             "config": {"workload": workload_label(args.workload, args.model, args.m), "global_batch": gb,
                        "per_gpu_batch": nb, "model": args.model, "m": args.m,
                        "macs_per_step": total_macs, "parallelism": f"dp{world}",
+                       "activation_zero_fraction": zero_frac,
                        "l2": l2_note,
                        "cuda_graph": use_graph},
             "clocks": clk,
@@ -658,6 +743,7 @@ def main():
                          "per_kind_ms_per_step": {k: v[0] / args.steps for k, v in kinds.items()},
                          "per_kind_gmacs": {k: v[1] / (v[0] * 1e-3) / 1e9 for k, v in kinds.items()}},
             "cpu_baseline": cpu,
+            "exact_bf16_step": exact_step,
             "full_train_step": full,
         }
         print(json.dumps(line), flush=True)

@@ -46,6 +46,9 @@ namespace dev {
 #ifndef AMSIM_PACK8
 #define AMSIM_PACK8 0
 #endif
+#ifndef AMSIM_DA
+#define AMSIM_DA 1   // interleave the decode of k-tile g+1 with the fast-path lookups of k-tile g
+#endif
 
 constexpr int BK = 16;
 constexpr int STAGES = 3;
@@ -574,16 +577,13 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
 // tracks min / max exponent fields over nonzero elements.
 // PACK: one word per element, alpha (bits 31..23) | offset (bits 22..0; shared
 // memory table offsets are < 2^18), halving the inner loop's operand loads.
-template <int NT, int ROWS, bool RAW_ALPHA = false, bool PACK = false>
-__device__ __forceinline__ void decode_operand(const float *raw, int kcontig, int cbl, uint32_t *al, uint32_t *off,
-                                               int shift, uint32_t mask, int off_shift, uint32_t off_base,
-                                               uint32_t &emin, uint32_t &emax, uint32_t elo, uint32_t ehi)
+template <int ROWS, bool RAW_ALPHA = false, bool PACK = false>
+__device__ __forceinline__ void decode_elem(const float *raw, int kcontig, int cbl, int e, uint32_t *al, uint32_t *off,
+                                            int shift, uint32_t mask, int off_shift, uint32_t off_base,
+                                            uint32_t &emin, uint32_t &emax, uint32_t elo, uint32_t ehi)
 {
-    constexpr int total = BK * ROWS;
-#pragma unroll
-    for (int e0 = 0; e0 < total; e0 += NT) {
-        const int e = e0 + threadIdx.x;
-        if (total % NT == 0 || e < total) {
+    {
+        {
             const int kk = e / ROWS, i = e % ROWS;
             float v;
             if (kcontig == 2) {  // TMA tile [ROWS][BK] with the 64-byte swizzle: 16-B chunk ^= address bits 8..7
@@ -612,6 +612,21 @@ __device__ __forceinline__ void decode_operand(const float *raw, int kcontig, in
                 emax = max(emax, ex);
             }
         }
+    }
+}
+
+template <int NT, int ROWS, bool RAW_ALPHA = false, bool PACK = false>
+__device__ __forceinline__ void decode_operand(const float *raw, int kcontig, int cbl, uint32_t *al, uint32_t *off,
+                                               int shift, uint32_t mask, int off_shift, uint32_t off_base,
+                                               uint32_t &emin, uint32_t &emax, uint32_t elo, uint32_t ehi)
+{
+    constexpr int total = BK * ROWS;
+#pragma unroll
+    for (int e0 = 0; e0 < total; e0 += NT) {
+        const int e = e0 + threadIdx.x;
+        if (total % NT == 0 || e < total)
+            decode_elem<ROWS, RAW_ALPHA, PACK>(raw, kcontig, cbl, e, al, off, shift, mask, off_shift, off_base, emin,
+                                               emax, elo, ehi);
     }
 }
 
@@ -873,11 +888,60 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     };
     for (int s = 0; s < STAGES - 1; s++) issue_next();
 
+    // Decode-ahead: k-tile g+1 is decoded into the other (alpha, offset) buffer
+    // -- interleaved with the lookups of k-tile g on the fast path -- and its
+    // exponent ranges are published before the one barrier per k-tile, so the
+    // decode's shared-memory latency hides behind the lookups instead of
+    // stalling the whole CTA between k-tiles.
+    static_assert((BK * BM) % NT == 0 && (BK * BN) % NT == 0, "decode work must split evenly over the threads");
+    constexpr int NEA = BK * BM / NT, NEB = BK * BN / NT;        // elements per thread and k-tile
+    constexpr int QA = (NEA + BK - 1) / BK, QB = (NEB + BK - 1) / BK; // ... per kk step of the fast loop
+    // Interleaving pays for the transposed orientation's 16-row tiles (Big^T /
+    // Flat^T / Huge^T: 1.5-3.5 % faster on dense operands, neutral on layer
+    // inputs) and costs 2-7 % in the normal orientation's zero-row-skipping
+    // loop and for 8-row tiles (tools/cfg_sweep.py with AMSIM_DA = 0 / 1,
+    // profiles/r02_cfg_da*.jsonl); elsewhere k-tile g+1 is decoded after the
+    // lookups of k-tile g, before the barrier.
+    constexpr bool DA = AMSIM_DA != 0 && TRN && TM == 16 && TN % 4 == 0 && MUL == MUL_LUT;
+    auto dec_a = [&](int gg) { return dec + (gg & 1) * Cf::DEC; };
+    auto raw_of = [&](int gg) { return raw + (gg % STAGES) * Cf::RAW_STAGE; };
+    auto wait_raw = [&](int gg) { mbar_wait(smem_u32(&bars[gg % STAGES]), uint32_t((gg / STAGES) & 1)); };
+    auto dec_one_a = [&](int gg, int i, uint32_t &mn, uint32_t &mx) {
+        uint32_t *d = dec_a(gg);
+        decode_elem<BM, MUL == MUL_NATIVE, PK>(raw_of(gg), p.da.kcontig, p.da.cblk_log2, i * NT + tid, d, d + BK * BM,
+                                               shift, mask, a_off_shift, a_off_base, mn, mx, elo, ehi);
+    };
+    auto dec_one_b = [&](int gg, int i, uint32_t &mn, uint32_t &mx) {
+        uint32_t *d = dec_a(gg) + 2 * BK * BM;
+        decode_elem<BN, MUL == MUL_NATIVE, PK>(raw_of(gg) + Cf::RAW_A, p.db.kcontig, p.db.cblk_log2, i * NT + tid, d,
+                                               d + BK * BN, shift, mask, b_off_shift, b_off_base, mn, mx, elo, ehi);
+    };
+    auto publish = [&](int gg, uint32_t amin, uint32_t amax, uint32_t bmin, uint32_t bmax) {
+        amin = __reduce_min_sync(0xffffffffu, amin);
+        amax = __reduce_max_sync(0xffffffffu, amax);
+        bmin = __reduce_min_sync(0xffffffffu, bmin);
+        bmax = __reduce_max_sync(0xffffffffu, bmax);
+        if (lane == 0) wflags[(gg & 1) * NWARPS + warp] = amin | (amax << 8) | (bmin << 16) | (bmax << 24);
+    };
+    auto decode_all = [&](int gg) {
+        uint32_t amin = 255, amax = 0, bmin = 255, bmax = 0;
+#pragma unroll
+        for (int i = 0; i < NEA; i++) dec_one_a(gg, i, amin, amax);
+#pragma unroll
+        for (int i = 0; i < NEB; i++) dec_one_b(gg, i, bmin, bmax);
+        publish(gg, amin, amax, bmin, bmax);
+    };
+
     float acc[TM][TN];
     uint32_t ecur[TN];   // SKIP: last entry loaded per column
 #pragma unroll
     for (int c = 0; c < TN; c++) ecur[c] = 0;
     int g = 0;
+    if (ig > 0) {   // the CTA's first k-tile
+        wait_raw(0);
+        decode_all(0);
+        __syncthreads();
+    }
     Sched CS;
     sched_start(CS);
     for (; CS.u.t >= 0; sched_next(CS)) {
@@ -890,25 +954,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 
         for (int kt = 0; kt < KT; kt++, g++) {
             issue_next();
-            const int stage = g % STAGES;
-            mbar_wait(smem_u32(&bars[stage]), uint32_t((g / STAGES) & 1));
-            const float *ra = raw + stage * Cf::RAW_STAGE;
-            const float *rb = ra + Cf::RAW_A;
-            uint32_t *d = dec + (g & 1) * Cf::DEC;
+            const bool has_next = ig > g + 1;   // k-tile g+1 exists (the issue cursor has issued it)
+            uint32_t *d = dec_a(g);
             uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + 2 * BK * BM, *b_off = b_al + BK * BN;
-            uint32_t amin = 255, amax = 0, bmin = 255, bmax = 0;
-            decode_operand<NT, BM, MUL == MUL_NATIVE, PK>(ra, p.da.kcontig, p.da.cblk_log2, a_al, a_off, shift, mask, a_off_shift,
-                                                          a_off_base, amin, amax, elo, ehi);
-            decode_operand<NT, BN, MUL == MUL_NATIVE, PK>(rb, p.db.kcontig, p.db.cblk_log2, b_al, b_off, shift, mask, b_off_shift,
-                                                          b_off_base, bmin, bmax, elo, ehi);
-            amin = __reduce_min_sync(0xffffffffu, amin);
-            amax = __reduce_max_sync(0xffffffffu, amax);
-            bmin = __reduce_min_sync(0xffffffffu, bmin);
-            bmax = __reduce_max_sync(0xffffffffu, bmax);
-            uint32_t *wf = wflags + (g & 1) * NWARPS;
-            if (lane == 0) wf[warp] = amin | (amax << 8) | (bmin << 16) | (bmax << 24);
-            __syncthreads();
-
+            const uint32_t *wf = wflags + (g & 1) * NWARPS;
             uint32_t lo = 0xFFFFFFFFu, hi = 0u;  // byte-wise mins (bytes 0, 2), maxs (bytes 1, 3)
 #pragma unroll
             for (int w = 0; w < NWARPS; w++) {
@@ -924,6 +973,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             // nonzero elements of the two smem tiles (conservative).
             const bool fast = p.policy == 0 && Amax <= 254 && Bmax <= 253 &&
                               (Amax == 0 || Bmax == 0 || (Amin + Bmin >= 128 && Amax + Bmax <= 380));
+            if (has_next) wait_raw(g + 1);
+            uint32_t namin = 255, namax = 0, nbmin = 255, nbmax = 0;   // k-tile g+1's exponent ranges (fast path)
 
             const uint32_t *A_al = a_al + Cf::wrow(warp), *A_off = a_off + Cf::wrow(warp);
             // lane columns: groups of 4 consecutive columns, group g at g * 128
@@ -957,6 +1008,14 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             } else if (fast) {
 #pragma unroll KK_UNROLL
                 for (int kk = 0; kk < BK; kk++) {
+                    if (DA && has_next) {   // decode-ahead slice of k-tile g+1
+#pragma unroll
+                        for (int q = 0; q < QA; q++)
+                            if (kk * QA + q < NEA) dec_one_a(g + 1, kk * QA + q, namin, namax);
+#pragma unroll
+                        for (int q = 0; q < QB; q++)
+                            if (kk * QB + q < NEB) dec_one_b(g + 1, kk * QB + q, nbmin, nbmax);
+                    }
                     uint32_t aal[TM], aof[TM], bal[TN], bof[TN], mul[TN];
 #pragma unroll
                     for (int r = 0; r < TM; r += 4) {
@@ -1050,6 +1109,12 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     }
                 }
             }
+            if (has_next) {
+                if (MUL == MUL_NATIVE || !fast || !DA) decode_all(g + 1);   // not interleaved
+                else publish(g + 1, namin, namax, nbmin, nbmax);
+            }
+            // k-tile g+1 decoded and published; dec[g & 1] and raw stage g free
+            __syncthreads();
         }
 
         const SubP &S = p.sub[T.s];

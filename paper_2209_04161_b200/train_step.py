@@ -74,6 +74,25 @@ class TrainStep:
         self.reducer = GradAllReducer(self.flat_grad, buckets, group=group, comm_stream=self.comm_stream)
         self.timers = None
 
+    def set_lut(self, lut):
+        """Run the same step with another table (e.g. the fully pinned exact
+        bf16 table next to MBM); grows the wgrad workspace if its plans need more."""
+        import torch
+        self.lut = lut
+        need = max(L.amsim_conv2d_bwd_filter_workspace(lut, ly.desc) // 4 for ly in self.layers if ly.kind == "conv")
+        if need > self.workspace.numel():
+            self.workspace = torch.empty(need, device=self.device)
+
+    def activation_zero_fraction(self) -> float:
+        """Fraction of exact zeros in the layer inputs (the warp-shared A operand
+        of conv fwd / wgrad): zero-row skipping saves their lookups, so the fwd /
+        wgrad rates depend on it (ReLU(N(0,1)) inputs: about 1/2)."""
+        zeros = total = 0
+        for ly in self.layers:
+            zeros += int((ly.x == 0).sum().item())
+            total += ly.x.numel()
+        return zeros / max(total, 1)
+
     # ------------------------------------------------------------------
     def step_macs(self) -> int:
         return sum(l.spec.macs() * (2 if l.spec.first else 3) for l in self.layers)
