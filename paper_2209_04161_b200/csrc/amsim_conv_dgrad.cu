@@ -21,6 +21,12 @@ amsim_status amsim_conv2d_bwd_data(const amsim_lut *lut, const amsim_conv2d_desc
     init_geom(a.g, d);
     Problem pr;
     dgrad_phases(d, pr, a.ph);
+    // TMA boxes for both operands (setup_tma): dy as [pixels][K] (1x1 unpadded),
+    // im2col boxes (stride 1) or per-phase im2col boxes (stride 2); w taps as 3-D boxes
+    const bool one = d->R == 1 && d->S == 1 && d->pad_h == 0 && d->pad_w == 0;
+    const bool s1 = d->stride_h == 1 && d->stride_w == 1;
+    pr.tma_lanes = aligned16(dy) && aligned16(w) && d->K % BK == 0 &&
+                   (one || s1 || (pr.nsub <= MAX_PH_TMA && !(path_policy() & 32)));
     a.dy = dy;
     a.fK.init(uint32_t(d->K));
     b.w = w;
@@ -35,7 +41,7 @@ amsim_status amsim_conv2d_bwd_data(const amsim_lut *lut, const amsim_conv2d_desc
         int BM, BN, NT;
         size_t smem;
         cfg_shape(CfgId(p.cfg), BM, BN, NT, smem, 0);
-        a.ph_tma = encode_dgrad_phases(a, pr.nsub, p.trn ? BN : BM) ? 1 : 0;
+        a.ph_tma = encode_dgrad_phases(a, pr.nsub, std::min(p.trn ? BN : BM, 256)) ? 1 : 0;
     }
     bool v = d->K % 4 == 0;
     p.da = OpDesc{1, (v && aligned16(dy)) ? 2 : 0};

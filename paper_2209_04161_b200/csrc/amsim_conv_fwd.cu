@@ -23,6 +23,9 @@ amsim_status amsim_conv2d_fwd(const amsim_lut *lut, const amsim_conv2d_desc *d, 
     pr.N = d->K;
     pr.M[0] = d->N * g.OH * g.OW;
     pr.K[0] = d->R * d->S * d->C;
+    // TMA boxes for both operands (setup_tma): x as [pixels][C] (1x1 / stride 1 /
+    // unpadded) or im2col boxes of 16 channels, w as [k][Cout]
+    pr.tma_lanes = aligned16(x) && aligned16(w) && d->K % 4 == 0 && (is_1x1_s1(g) ? d->C % 4 == 0 : d->C % BK == 0);
     KParams p{};
     int eb = 32;
     s = prepare(lut, p, pr, eb);

@@ -498,8 +498,13 @@ struct DgW {
 
 // NT threads as WM x WN warps (WN = warps side by side along N); each warp owns
 // TM rows x 32*TN columns of the BM x BN CTA tile.
-template <int NT_, int TM_, int TN_, int WN_ = 1>
+// NP ("narrow"): raw tiles without row padding and one packed word per decoded
+// element -- only for launches whose operands are all TMA boxes (no k-contiguous
+// cp.async layout) with packed (16/32-bit shared) tables; lets the 64 x 512
+// tile (Flat8) fit shared memory.
+template <int NT_, int TM_, int TN_, int WN_ = 1, bool NP_ = false>
 struct KCfg {
+    static constexpr bool NP = NP_;
     static constexpr int NT = NT_;
     static constexpr int NWARPS = NT / 32;
     static constexpr int TM = TM_;
@@ -518,10 +523,10 @@ struct KCfg {
     static constexpr bool G4 = TN % 4 == 0;
     static constexpr int CG = G4 ? 4 : TN;
     static constexpr __host__ __device__ int col(int c) { return G4 ? (c >> 2) * 128 + (c & 3) : c; }
-    static constexpr int RAW_A = BM * (BK + RAW_PAD);
-    static constexpr int RAW_B = BN * (BK + RAW_PAD);
+    static constexpr int RAW_A = BM * (BK + (NP ? 0 : RAW_PAD));
+    static constexpr int RAW_B = BN * (BK + (NP ? 0 : RAW_PAD));
     static constexpr int RAW_STAGE = RAW_A + RAW_B;        // floats
-    static constexpr int DEC = 2 * BK * (BM + BN);         // u32 per buffer (alpha + offset)
+    static constexpr int DEC = (NP ? 1 : 2) * BK * (BM + BN);   // u32 per buffer (alpha + offset, or packed)
     static size_t smem_bytes(uint32_t lut_bytes)
     {
         size_t lut = (lut_bytes + 127) & ~size_t(127);
@@ -858,16 +863,22 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     auto load_op = [&](int mode, const CUtensorMap *map, uint32_t dst, const auto &op, int mn0,
                                        int rows, int cbl) {
                         if (mode == 6) {   // per-phase im2col descriptor held by the operand map
-                            op.tma_coords(IT.s, mn0, k0, c);
-                            load(4, phase_map(op, IT.s, map), dst);
+                            for (int j = 0; j < rows; j += 256) {
+                                op.tma_coords(IT.s, mn0 + j, k0, c);
+                                load(4, phase_map(op, IT.s, map), dst + uint32_t(j * BK) * 4u);
+                            }
                         } else if (mode == 5) {
                             for (int t = 0; t < (rows >> cbl); t++) {
                                 op.tma_coords(IT.s, mn0 + (t << cbl), k0, c);
                                 load(4, map, dst + uint32_t(t * (BK << cbl)) * 4u);
                             }
                         } else {
-                            op.tma_coords(IT.s, mn0, k0, c);
-                            load(mode, map, dst);
+                            // a box holds <= 256 rows: taller tiles (k-contiguous [rows][BK] only) take
+                            // several boxes, 256 rows (16 KB, a multiple of the swizzle span) apart
+                            for (int j = 0; j < rows; j += 256) {
+                                op.tma_coords(IT.s, mn0 + j, k0, c);
+                                load(mode, map, dst + uint32_t(j * BK) * 4u);
+                            }
                         }
                     };
                     if (p.tma_on[0]) load_op(p.tma_on[0], &p.tma[0], smem_u32(ra), opa, IT.m0, BM, p.da.cblk_log2);
@@ -903,6 +914,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // profiles/r02_cfg_da*.jsonl); elsewhere k-tile g+1 is decoded after the
     // lookups of k-tile g, before the barrier.
     constexpr bool DA = AMSIM_DA != 0 && TRN && TM == 16 && TN % 4 == 0 && MUL == MUL_LUT;
+    static_assert(!Cf::NP || PK, "narrow (NP) tile configurations need the packed operand words");
+    constexpr int DSTR = PK ? 1 : 2;   // decoded words per element (packed: alpha | offset)
     auto dec_a = [&](int gg) { return dec + (gg & 1) * Cf::DEC; };
     auto raw_of = [&](int gg) { return raw + (gg % STAGES) * Cf::RAW_STAGE; };
     auto wait_raw = [&](int gg) { mbar_wait(smem_u32(&bars[gg % STAGES]), uint32_t((gg / STAGES) & 1)); };
@@ -912,7 +925,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                                                shift, mask, a_off_shift, a_off_base, mn, mx, elo, ehi);
     };
     auto dec_one_b = [&](int gg, int i, uint32_t &mn, uint32_t &mx) {
-        uint32_t *d = dec_a(gg) + 2 * BK * BM;
+        uint32_t *d = dec_a(gg) + DSTR * BK * BM;
         decode_elem<BN, MUL == MUL_NATIVE, PK>(raw_of(gg) + Cf::RAW_A, p.db.kcontig, p.db.cblk_log2, i * NT + tid, d,
                                                d + BK * BN, shift, mask, b_off_shift, b_off_base, mn, mx, elo, ehi);
     };
@@ -956,7 +969,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             issue_next();
             const bool has_next = ig > g + 1;   // k-tile g+1 exists (the issue cursor has issued it)
             uint32_t *d = dec_a(g);
-            uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + 2 * BK * BM, *b_off = b_al + BK * BN;
+            uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + DSTR * BK * BM, *b_off = b_al + BK * BN;
             const uint32_t *wf = wflags + (g & 1) * NWARPS;
             uint32_t lo = 0xFFFFFFFFu, hi = 0u;  // byte-wise mins (bytes 0, 2), maxs (bytes 1, 3)
 #pragma unroll

@@ -98,7 +98,10 @@ using CfgFlat = KCfg<256, 16, 4, 2>;                     // 64 x 256: 64-row pro
                                                          // with Big's 16 x 4 register tile instead of Wide's 8 x 4
 using CfgTall = KCfg<256, 20, 2>;
 using CfgTallT = KCfg<256, 8, 5>;                        // 64 x 160, transposed only: 129..160 lanes (stem wgrad, 147)
-using CfgFlat3 = KCfg<256, 16, 3, 2>;                    // 64 x 192, transposed only: lanes = 576 = 3 x 192 (3x3 x 64-channel wgrad)                        // 160 x 64: 129..160-row problems (stem wgrad, M = 7*7*3)
+using CfgFlat3 = KCfg<256, 16, 3, 2>;                    // 64 x 192, transposed only: lanes = 576 = 3 x 192 (3x3 x 64-channel wgrad)
+using CfgFlat8 = KCfg<256, 16, 8, 2, true>;              // 64 x 512, transposed only: Huge's 16 x 8 register tile for
+                                                         // the 64-channel layers; narrow shared-memory layout (NP), so
+                                                         // both operands must be k-contiguous TMA boxes
 
 static int g_num_sms = 0;
 static int num_sms()
@@ -124,6 +127,9 @@ struct Problem {
     int nsub = 1;
     int M[MAX_SUB] = {0};
     int K[MAX_SUB] = {0};
+    // the original A operand (the lanes in the transposed orientation) is loaded
+    // as k-contiguous TMA boxes and B as TMA boxes: the narrow Flat8 tile may be used
+    bool tma_lanes = false;
     // the A operand is a layer input (ReLU activations in a network): in the
     // transposed orientation it is read by the lanes, where its zeros share one
     // table word and cut bank conflicts (measured +7 % on ResNet-50 l2.1.conv1
@@ -131,7 +137,7 @@ struct Problem {
     bool a_is_activation = false;
 };
 
-enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat, Tall, Flat3, TallT };
+enum class CfgId { Small, Mid, Big, Lean, Wide, Huge, Flat, Tall, Flat3, TallT, Flat8 };
 static constexpr size_t kSmemMax = 227 * 1024;
 
 static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t lut_bytes)
@@ -146,6 +152,7 @@ static void cfg_shape(CfgId c, int &BM, int &BN, int &NT, size_t &smem, uint32_t
     case CfgId::Tall: BM = CfgTall::BM; BN = CfgTall::BN; NT = CfgTall::NT; smem = CfgTall::smem_bytes(lut_bytes); break;
     case CfgId::TallT: BM = CfgTallT::BM; BN = CfgTallT::BN; NT = CfgTallT::NT; smem = CfgTallT::smem_bytes(lut_bytes); break;
     case CfgId::Flat3: BM = CfgFlat3::BM; BN = CfgFlat3::BN; NT = CfgFlat3::NT; smem = CfgFlat3::smem_bytes(lut_bytes); break;
+    case CfgId::Flat8: BM = CfgFlat8::BM; BN = CfgFlat8::BN; NT = CfgFlat8::NT; smem = CfgFlat8::smem_bytes(lut_bytes); break;
     default: BM = CfgBig::BM; BN = CfgBig::BN; NT = CfgBig::NT; smem = CfgBig::smem_bytes(lut_bytes); break;
     }
 }
@@ -246,6 +253,7 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
     case CfgId::Flat: TM = 16; TN = 4; break;
     case CfgId::Tall: TM = 20; TN = 2; break;
     case CfgId::Flat3: TM = 16; TN = 3; break;
+    case CfgId::Flat8: TM = 16; TN = 8; break;
     case CfgId::TallT: TM = 8; TN = 5; break;
     default: break;
     }
@@ -266,22 +274,23 @@ static double measured_cost16(CfgId c, bool trn, bool act)
 {
     if (trn) {
         switch (c) {
-        case CfgId::Huge: return act ? 0.2583 : 0.2752;
-        case CfgId::Big: return act ? 0.2812 : 0.2990;
-        case CfgId::Flat: return act ? 0.2866 : 0.3159;
-        case CfgId::Flat3: return act ? 0.3112 : 0.3229;
-        case CfgId::TallT: return act ? 0.3122 : 0.3340;
-        case CfgId::Wide: return act ? 0.3240 : 0.3462;
+        case CfgId::Huge: return act ? 0.2562 : 0.2699;
+        case CfgId::Big: return act ? 0.2749 : 0.2870;
+        case CfgId::Flat: return act ? 0.2866 : 0.2990;
+        case CfgId::Flat3: return act ? 0.3071 : 0.3222;
+        case CfgId::Flat8: return act ? 0.2562 : 0.2699;   // not yet measured: Huge^T's (same 16 x 8 register tile)
+        case CfgId::TallT: return act ? 0.3068 : 0.3236;
+        case CfgId::Wide: return act ? 0.3153 : 0.3385;
         default: return -1.0;
         }
     }
     switch (c) {
-    case CfgId::Huge: return act ? 0.2190 : 0.2732;
-    case CfgId::Big: return act ? 0.2649 : 0.3077;
-    case CfgId::Flat: return act ? 0.2705 : 0.3104;
-    case CfgId::Mid: return act ? 0.3487 : 0.3605;
-    case CfgId::Lean: return act ? 0.4236 : 0.4391;
-    case CfgId::Small: return act ? 0.5630 : 0.5970;
+    case CfgId::Huge: return act ? 0.2176 : 0.2689;
+    case CfgId::Big: return act ? 0.2652 : 0.3021;
+    case CfgId::Flat: return act ? 0.2702 : 0.3101;
+    case CfgId::Mid: return act ? 0.3399 : 0.3513;
+    case CfgId::Lean: return act ? 0.4039 : 0.4198;
+    case CfgId::Small: return act ? 0.5517 : 0.5769;
     // offered only for <= 64 (Wide) / 129..160 rows (Tall), absent from the sweep's
     // shapes: Tall from the r01 stem-wgrad ratio to TallT^T (1.093), Wide between
     // Big and Wide^T
@@ -298,10 +307,12 @@ static int cfg_tn(CfgId c)
     case CfgId::Mid: case CfgId::Lean: case CfgId::Tall: return 2;
     case CfgId::Flat3: return 3;
     case CfgId::TallT: return 5;
-    case CfgId::Huge: return 8;
+    case CfgId::Huge: case CfgId::Flat8: return 8;
     default: return 4;
     }
 }
+
+static bool tma_disabled() { return (path_policy() & 8) != 0; }   // policy bit 3: cp.async for every operand
 
 // Plan cache: the same problem (shape, table width, mode, policy) is planned
 // once per process.
@@ -356,8 +367,8 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
     if (const char *f = std::getenv("AMSIM_SCHED"); f && *f) sched = f[0];
     // lut->symmetric decides whether the transposed orientation (which reads
     // LUT^T) may be planned, so it is part of the key
-    std::vector<int64_t> key = {pr.N, pr.nsub, pr.a_is_activation, eb, p.lut_global, p.mul, policy & (3 | 16), mbits,
-                                num_sms(), force, lut->symmetric ? 1 : 0, sched};
+    std::vector<int64_t> key = {pr.N, pr.nsub, pr.a_is_activation, eb, p.lut_global, p.mul, policy & (3 | 8 | 16 | 32),
+                                mbits, num_sms(), force, lut->symmetric ? 1 : 0, sched, pr.tma_lanes ? 1 : 0};
     for (int i = 0; i < pr.nsub; i++) {
         key.push_back(pr.M[i]);
         key.push_back(pr.K[i]);
@@ -449,7 +460,11 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         if (pr.M[0] % CfgFlat3::BN == 0 && pr.M[0] % CfgFlat::BN != 0) tc.push_back(CfgId::Flat3);
         if (pr.M[0] > 128 && pr.M[0] <= CfgTallT::BN) tc.push_back(CfgId::TallT);
         if (eb >= 16) tc.push_back(CfgId::Huge);
+        // 64 x 512 for <= 64 output channels when every operand tile is a TMA box
+        if (eb == 16 && pr.tma_lanes && !tma_disabled() && pr.N <= 64) tc.push_back(CfgId::Flat8);
         if (force >= 10) tc = {CfgId(force - 10)};
+        if (force >= 10 && CfgId(force - 10) == CfgId::Flat8 && !(eb == 16 && pr.tma_lanes && !tma_disabled()))
+            tc = {CfgId::Flat};
         if (force >= 10 && CfgId(force - 10) == CfgId::Huge && eb < 16) tc = {CfgId::Big};
         for (CfgId c : tc) {
             int BM, BN, NT;
@@ -583,7 +598,6 @@ static int encode_tma(CUtensorMap *map, const float *base, int rank, const cuuin
     return r == CUDA_SUCCESS ? rank : 0;
 }
 
-static bool tma_disabled() { return (path_policy() & 8) != 0; }   // policy bit 3: cp.async for every operand
 
 static PFN_cuTensorMapEncodeIm2col_v12000 tma_im2col_fn()
 {
@@ -757,6 +771,9 @@ static amsim_status launch_trn(const KParams &p, const OpR &r, const OpC &c, cud
     case CfgId::Wide: return launch_cfg<CfgWide, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Flat: return launch_cfg<CfgFlat, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Flat3: return launch_cfg<CfgFlat3, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
+    case CfgId::Flat8:
+        if constexpr (EB == 16) return launch_cfg<CfgFlat8, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
+        else break;
     case CfgId::TallT: return launch_cfg<CfgTallT, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Big: return launch_cfg<CfgBig, EB, OpR, OpC, false, MUL_LUT, true>(p, r, c, st);
     case CfgId::Huge:
@@ -797,8 +814,13 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
     amsim_status s;
     if (p.trn) {   // rows = original B operand, lanes = original A operand
         std::swap(p.da, p.db);
-        p.tma_on[0] = setup_tma(&p.tma[0], b, BM, p.da);
-        p.tma_on[1] = setup_tma(&p.tma[1], a, BN, p.db);
+        p.tma_on[0] = setup_tma(&p.tma[0], b, std::min(BM, 256), p.da);
+        p.tma_on[1] = setup_tma(&p.tma[1], a, std::min(BN, 256), p.db);   // taller tiles: several boxes
+        if (CfgId(p.cfg) == CfgId::Flat8 &&
+            !(p.tma_on[0] && p.tma_on[1] && p.da.kcontig != 1 && p.db.kcontig == 2 && p.tma_on[1] != 5)) {
+            if (own) scratch_free(ws, st);
+            return set_error(AMSIM_ERR_UNSUPPORTED, "internal: the 64 x 512 tile needs TMA-staged operands");
+        }
         s = eb == 8 ? launch_trn<8>(p, b, a, st) : launch_trn<16>(p, b, a, st);
     } else {
         p.tma_on[0] = setup_tma(&p.tma[0], a, BM, p.da);

@@ -39,6 +39,8 @@ amsim_status amsim_gemm(const amsim_lut *lut, int trans_a, int trans_b, int64_t 
     pr.N = int(N);
     pr.M[0] = int(M);
     pr.K[0] = int(K);
+    // TMA boxes for both operands, A k-contiguous (setup_tma)
+    pr.tma_lanes = !trans_a && aligned16(A) && aligned16(B) && lda % 4 == 0 && ldb % 4 == 0;
     KParams p{};
     int eb = 32;
     amsim_status s = prepare(lut, p, pr, eb);

@@ -888,7 +888,7 @@ def test_transposed_orientation_equals_normal(am, luts, orc, model):
     assert_tol(outs[16][0], res, "gemm split, normal orientation")
 
 
-@pytest.mark.parametrize("force", ["14", "12", "15", "16", "18", "19", "6"])
+@pytest.mark.parametrize("force", ["14", "12", "15", "16", "18", "19", "6", "20"])
 def test_transposed_orientation_forced(am, luts, orc, force, monkeypatch):
     """Every pass in the transposed orientation (AMSIM_FORCE_CFG >= 10 forces
     it wherever it is allowed), cp.async operand gathers (C % BN != 0) and TMA
@@ -942,7 +942,7 @@ def test_wgrad_multi_tap_tma(am, luts, orc, force, monkeypatch):
         assert_tol(_run_conv(am, lut, d, x, w, dy, "wgrad"), want, f"{shape} split")
 
 
-@pytest.mark.parametrize("force", [None, "2", "5", "16", "15"])
+@pytest.mark.parametrize("force", [None, "2", "5", "16", "15", "20"])
 def test_strided_dgrad_phase_tma(am, luts, orc, force, monkeypatch):
     """Stride-2 dgrad reads dy through one im2col TMA descriptor per stride
     phase (lower corner from the phase's first tap, upper from its extent):
@@ -1236,3 +1236,33 @@ def test_stream_k_transposed_and_forced_configs(am, luts, orc, monkeypatch):
         monkeypatch.setenv("AMSIM_FORCE_CFG", force)
         for which, ref in refs.items():
             assert_tol(_run_conv(am, lut, d, x, w, dy, which), ref, f"force={force} {which}")
+
+
+@pytest.mark.parametrize("policy", [0, 8, 32])
+def test_flat8_narrow_tile(am, luts, orc, policy, monkeypatch):
+    """The 64 x 512 transposed tile (AMSIM_FORCE_CFG=20, narrow shared-memory
+    layout, lane tiles loaded as two 256-row TMA boxes): conv fwd and dgrad of
+    64-channel layers -- 3x3 stride 1 (im2col boxes), stride 2 (per-phase
+    boxes), 1x1 (2-D boxes) -- with pixel counts that leave ragged 512-lane
+    tiles; bits in exact order, tolerance in the default plan.  Policy bits 3 /
+    5 (cp.async gathers) make the planner fall back to a padded tile."""
+    monkeypatch.setenv("AMSIM_FORCE_CFG", "20")
+    lut = luts("mbm")
+    for k, shape in enumerate([(3, 15, 15, 64, 64, 3, 3, 1, 1), (2, 23, 23, 64, 64, 3, 3, 2, 1),
+                               (3, 14, 13, 256, 64, 1, 1, 1, 0), (2, 17, 17, 64, 48, 1, 1, 2, 0)]):
+        x, w, dy, OH, OW = _conv_tensors(shape, 230 + k)
+        d, od = am.conv_desc(*shape), orc.conv_desc(*shape)
+        refs = {"fwd": orc.conv_fwd(od, x, w, "mbm"), "dgrad": orc.conv_bwd_data(od, dy, w, "mbm")}
+        for which, ref in refs.items():
+            am.amsim_set_path_policy(policy | 2)
+            try:
+                got = _run_conv(am, lut, d, x, w, dy, which)
+            finally:
+                am.amsim_set_path_policy(0)
+            assert_bits(got, ref.c32, f"{shape} {which} policy {policy} (exact order)")
+            am.amsim_set_path_policy(policy)
+            try:
+                got = _run_conv(am, lut, d, x, w, dy, which)
+            finally:
+                am.amsim_set_path_policy(0)
+            assert_tol(got, ref, f"{shape} {which} policy {policy}")

@@ -17,10 +17,10 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-CFGS = ["auto", "0", "1", "2", "3", "4", "5", "6", "7", "12", "14", "15", "16", "18", "19"]
+CFGS = ["auto", "0", "1", "2", "3", "4", "5", "6", "7", "12", "14", "15", "16", "18", "19", "20"]
 NAMES = {"0": "Small", "1": "Mid", "2": "Big", "3": "Lean", "4": "Wide", "5": "Huge",
          "6": "Flat", "7": "Tall",
-         "12": "Big^T", "14": "Wide^T", "15": "Huge^T", "16": "Flat^T", "18": "Flat3^T", "19": "TallT^T", "auto": "auto"}
+         "12": "Big^T", "14": "Wide^T", "15": "Huge^T", "16": "Flat^T", "18": "Flat3^T", "19": "TallT^T", "20": "Flat8^T", "auto": "auto"}
 
 
 def main():
