@@ -535,6 +535,11 @@ struct KCfg {
     }
 };
 
+// dgrad operand maps (dense error operands: no zero-row skipping to protect)
+template <class Op> struct is_dgrad_op { static constexpr bool value = false; };
+template <> struct is_dgrad_op<DgDY> { static constexpr bool value = true; };
+template <> struct is_dgrad_op<DgW> { static constexpr bool value = true; };
+
 // Descriptor of sub-problem s: the operand's own per-phase map (DgDY, mode 6)
 // or the launch-wide one.
 template <class Op>
@@ -909,11 +914,14 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     constexpr int QA = (NEA + BK - 1) / BK, QB = (NEB + BK - 1) / BK; // ... per kk step of the fast loop
     // Interleaving pays for the transposed orientation's 16-row tiles (Big^T /
     // Flat^T / Huge^T: 1.5-3.5 % faster on dense operands, neutral on layer
-    // inputs) and costs 2-7 % in the normal orientation's zero-row-skipping
-    // loop and for 8-row tiles (tools/cfg_sweep.py with AMSIM_DA = 0 / 1,
+    // inputs) and for the normal 16 x 8 tile on dense errors (dgrad, 1 %); it
+    // costs 2-7 % in the normal orientation's zero-row-skipping loop on layer
+    // inputs and for 8-row tiles (tools/cfg_sweep.py with AMSIM_DA = 0 / 1,
     // profiles/r02_cfg_da*.jsonl); elsewhere k-tile g+1 is decoded after the
     // lookups of k-tile g, before the barrier.
-    constexpr bool DA = AMSIM_DA != 0 && TRN && TM == 16 && TN % 4 == 0 && MUL == MUL_LUT;
+    constexpr bool DGRAD = is_dgrad_op<OpA>::value || is_dgrad_op<OpB>::value;   // dense operands (errors)
+    constexpr bool DA = AMSIM_DA != 0 && MUL == MUL_LUT && TM == 16 &&
+                        (TRN ? TN % 4 == 0 : (DGRAD && TN == 8));
     static_assert(!Cf::NP || PK, "narrow (NP) tile configurations need the packed operand words");
     constexpr int DSTR = PK ? 1 : 2;   // decoded words per element (packed: alpha | offset)
     auto dec_a = [&](int gg) { return dec + (gg & 1) * Cf::DEC; };
@@ -1196,11 +1204,27 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                 int row = T.m0 + Cf::wrow(warp) + r;
                 if (row >= S.M) continue;
                 float *dst = p.C + opa.out_row(T.s, row, p.ldc);
+                if constexpr (Cf::G4) {
+                    // a lane's 4-column groups are contiguous: one 16-byte store per group
 #pragma unroll
-                for (int c = 0; c < TN; c++) {
-                    int col = T.n0 + Cf::wcol(warp) + lane * CG + Cf::col(c);
-                    if (col >= p.N) continue;
-                    dst[col] = p.accumulate ? (dst[col] + acc[r][c]) : acc[r][c];
+                    for (int c = 0; c < TN; c += 4) {
+                        const int col = T.n0 + Cf::wcol(warp) + lane * CG + Cf::col(c);
+                        float *q = dst + col;
+                        if (col + 3 < p.N && !p.accumulate && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+                            *reinterpret_cast<float4 *>(q) = make_float4(acc[r][c], acc[r][c + 1], acc[r][c + 2], acc[r][c + 3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; j++)
+                                if (col + j < p.N) q[j] = p.accumulate ? (q[j] + acc[r][c + j]) : acc[r][c + j];
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < TN; c++) {
+                        int col = T.n0 + Cf::wcol(warp) + lane * CG + Cf::col(c);
+                        if (col >= p.N) continue;
+                        dst[col] = p.accumulate ? (dst[col] + acc[r][c]) : acc[r][c];
+                    }
                 }
             }
         }
