@@ -46,6 +46,14 @@ namespace dev {
 #ifndef AMSIM_PACK8
 #define AMSIM_PACK8 0
 #endif
+#ifndef AMSIM_ROWPRED
+#define AMSIM_ROWPRED 0   // zero-row skipping: one predicate per row (lut_row_if16) instead of per lookup
+                          // (fewer SASS instructions, but measured 0.7 % slower on the step: off)
+#endif
+#ifndef AMSIM_DGRAD_SKIP
+#define AMSIM_DGRAD_SKIP 1   // zero-row skipping also in the dgrad kernels (dense errors; measured 0.4 %
+                             // faster on dgrad than the plain lookups, same box, tools/ab_bench.py)
+#endif
 #ifndef AMSIM_DA
 #define AMSIM_DA 1   // interleave the decode of k-tile g+1 with the fast-path lookups of k-tile g
 #endif
@@ -171,6 +179,31 @@ __device__ __forceinline__ void lut_entry_if(uint32_t &v, uint32_t addr, uint32_
     else
         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
                      : "+r"(v) : "r"(addr), "r"(act));
+}
+
+// One warp-shared row's TN lookups (TN = 4 or 8, 16-bit entries), all
+// predicated on the row's A element being nonzero (`act` != 0): one predicate
+// per row instead of one per lookup; an inactive row keeps v[] unchanged.
+template <int TN>
+__device__ __forceinline__ void lut_row_if16(uint32_t (&v)[TN], const uint32_t (&a)[TN], uint32_t act)
+{
+    static_assert(TN == 4 || TN == 8, "row-predicated lookups for 4 or 8 columns");
+    if constexpr (TN == 4) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %8, 0;\n\t"
+                     "@q ld.shared.u16 %0, [%4];\n\t@q ld.shared.u16 %1, [%5];\n\t"
+                     "@q ld.shared.u16 %2, [%6];\n\t@q ld.shared.u16 %3, [%7];\n\t}"
+                     : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3])
+                     : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(act));
+    } else {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %16, 0;\n\t"
+                     "@q ld.shared.u16 %0, [%8];\n\t@q ld.shared.u16 %1, [%9];\n\t"
+                     "@q ld.shared.u16 %2, [%10];\n\t@q ld.shared.u16 %3, [%11];\n\t"
+                     "@q ld.shared.u16 %4, [%12];\n\t@q ld.shared.u16 %5, [%13];\n\t"
+                     "@q ld.shared.u16 %6, [%14];\n\t@q ld.shared.u16 %7, [%15];\n\t}"
+                     : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
+                     : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]),
+                       "r"(act));
+    }
 }
 
 // Table entry at byte offset `addr`: a shared-memory address (GL = false) or
@@ -701,7 +734,11 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // Only for TN >= 4: the per-row predicate costs one LOP3 per row and k,
     // which 1- and 2-column tiles cannot amortise (LeNet-5: +17 % measured).
     constexpr int KK_UNROLL = TM * TN <= 64 ? AMSIM_KK_UNROLL_SMALL : 2;
-    constexpr bool SKIP = AMSIM_SKIP && MUL == MUL_LUT && !GL && EB >= 16 && !TRN && TN >= 4;
+    // dgrad's A operand is the layer error (dense): AMSIM_DGRAD_SKIP = 0 would
+    // give its kernels the plain lookups (measured slower, so off)
+    constexpr bool DGRAD = is_dgrad_op<OpA>::value || is_dgrad_op<OpB>::value;
+    constexpr bool SKIP = AMSIM_SKIP && MUL == MUL_LUT && !GL && EB >= 16 && !TRN && TN >= 4 && (!DGRAD || AMSIM_DGRAD_SKIP);
+    constexpr bool ROWPRED = SKIP && AMSIM_ROWPRED && EB == 16 && (TN == 4 || TN == 8);
     constexpr uint32_t AMASK = 0xFF800000u, OMASK = 0x007FFFFFu;
     extern __shared__ __align__(128) unsigned char smem[];
 
@@ -919,7 +956,6 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // inputs and for 8-row tiles (tools/cfg_sweep.py with AMSIM_DA = 0 / 1,
     // profiles/r02_cfg_da*.jsonl); elsewhere k-tile g+1 is decoded after the
     // lookups of k-tile g, before the barrier.
-    constexpr bool DGRAD = is_dgrad_op<OpA>::value || is_dgrad_op<OpB>::value;   // dense operands (errors)
     constexpr bool DA = AMSIM_DA != 0 && MUL == MUL_LUT && TM == 16 &&
                         (TRN ? TN % 4 == 0 : (DGRAD && TN == 8));
     static_assert(!Cf::NP || PK, "narrow (NP) tile configurations need the packed operand words");
@@ -1082,11 +1118,19 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 #pragma unroll
                     for (int c = 0; c < TN; c++) mul[c] = min(bal[c] << 1, MULV);
 #pragma unroll
-                    for (int r = 0; r < TM; r++)
+                    for (int r = 0; r < TM; r++) {
+                        if constexpr (ROWPRED) {
+                            uint32_t ad[TN];
+#pragma unroll
+                            for (int c = 0; c < TN; c++) ad[c] = aof[r] + bof[c];
+                            lut_row_if16<TN>(ecur, ad, aal[r] << 1);
+                        }
 #pragma unroll
                         for (int c = 0; c < TN; c++) {
                             uint32_t e;
-                            if constexpr (SKIP) {
+                            if constexpr (ROWPRED) {
+                                e = ecur[c];
+                            } else if constexpr (SKIP) {
                                 lut_entry_if<EB>(ecur[c], aof[r] + bof[c], aal[r] << 1);
                                 e = ecur[c];
                             } else {
@@ -1096,6 +1140,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                             uint32_t x = e * mul[c] + bal[c];
                             acc[r][c] = fma_ftz(__uint_as_float(x), __uint_as_float(aal[r]), acc[r][c]);
                         }
+                    }
                 }
             } else {
                 // careful path: Alg. 2 literally, readings C4-C7
