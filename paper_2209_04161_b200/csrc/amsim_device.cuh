@@ -54,6 +54,12 @@ namespace dev {
 #define AMSIM_DGRAD_SKIP 1   // zero-row skipping also in the dgrad kernels (dense errors; measured 0.4 %
                              // faster on dgrad than the plain lookups, same box, tools/ab_bench.py)
 #endif
+#ifndef AMSIM_DECODE_LATE
+// 1: every kernel decodes k-tile g right before its lookups (the round-1 order);
+// 0: only the 8-bit-table conv fwd / wgrad kernels (issue-bound on layer inputs:
+// measured 2-3 % faster there, 1-2 % slower everywhere else, tools/ab_bench.py)
+#define AMSIM_DECODE_LATE 0
+#endif
 #ifndef AMSIM_DA
 #define AMSIM_DA 1   // interleave the decode of k-tile g+1 with the fast-path lookups of k-tile g
 #endif
@@ -573,6 +579,11 @@ template <class Op> struct is_dgrad_op { static constexpr bool value = false; };
 template <> struct is_dgrad_op<DgDY> { static constexpr bool value = true; };
 template <> struct is_dgrad_op<DgW> { static constexpr bool value = true; };
 
+// conv fwd / wgrad operand maps (layer inputs: ReLU zeros)
+template <class Op> struct is_act_op { static constexpr bool value = false; };
+template <> struct is_act_op<FwdX> { static constexpr bool value = true; };
+template <> struct is_act_op<WgX> { static constexpr bool value = true; };
+
 // Descriptor of sub-problem s: the operand's own per-phase map (DgDY, mode 6)
 // or the launch-wide one.
 template <class Op>
@@ -994,7 +1005,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 #pragma unroll
     for (int c = 0; c < TN; c++) ecur[c] = 0;
     int g = 0;
-    if (ig > 0) {   // the CTA's first k-tile
+    constexpr bool LATE = AMSIM_DECODE_LATE != 0 || (EB == 8 && MUL == MUL_LUT && (is_act_op<OpA>::value || is_act_op<OpB>::value));
+    if (!LATE && ig > 0) {   // the CTA's first k-tile
         wait_raw(0);
         decode_all(0);
         __syncthreads();
@@ -1011,7 +1023,12 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 
         for (int kt = 0; kt < KT; kt++, g++) {
             issue_next();
-            const bool has_next = ig > g + 1;   // k-tile g+1 exists (the issue cursor has issued it)
+            const bool has_next = !LATE && ig > g + 1;   // k-tile g+1 exists (the issue cursor has issued it)
+            if (LATE) {   // the round-1 order: this k-tile's decode, then the barrier, then its lookups
+                wait_raw(g);
+                decode_all(g);
+                __syncthreads();
+            }
             uint32_t *d = dec_a(g);
             uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + DSTR * BK * BM, *b_off = b_al + BK * BN;
             const uint32_t *wf = wflags + (g & 1) * NWARPS;
@@ -1180,7 +1197,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                 else publish(g + 1, namin, namax, nbmin, nbmax);
             }
             // k-tile g+1 decoded and published; dec[g & 1] and raw stage g free
-            __syncthreads();
+            if (!LATE) __syncthreads();
         }
 
         const SubP &S = p.sub[T.s];
