@@ -204,16 +204,28 @@ static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int polic
     // stream-K makespan: W / Gsk k-tiles, the per-unit overhead of the tiles a
     // range touches, partial tiles through HBM, and the last piece's fix-up
     // reading every piece of its tile
-    const int min_chunk = 4;   // k-tiles per CTA at least (small problems use fewer CTAs)
-    const int Gsk = int(std::max<int64_t>(1, std::min<int64_t>(G, W / min_chunk)));
-    const double per_cta = double(W) / Gsk;
-    const double units = double(p.ntiles) / Gsk + 1.0;
-    double pieces_max = 1.0;
-    for (int s = 0; s < pr.nsub; s++)
-        pieces_max = std::max(pieces_max, std::ceil(std::max(p.sub[s].kt, 1) / per_cta) + 1.0);
+    // small problems may use fewer CTAs than SMs (each at least `chunk` k-tiles):
+    // the count that minimises the modelled time
     const double tile_bytes = 4.0 * BM * BN;
-    const double sk = std::ceil(per_cta) + tile_overhead * units + 2.0 * 2.0 * Gsk * tile_bytes / hbm_per_unit +
-                      pieces_max * tile_bytes / l2_per_unit_sm;
+    auto sk_cost = [&](int g) {
+        const double per_cta = double(W) / g;
+        const double units = double(p.ntiles) / g + 1.0;
+        double pieces_max = 1.0;
+        for (int s = 0; s < pr.nsub; s++)
+            pieces_max = std::max(pieces_max, std::ceil(std::max(p.sub[s].kt, 1) / per_cta) + 1.0);
+        return std::ceil(per_cta) + tile_overhead * units + 2.0 * 2.0 * g * tile_bytes / hbm_per_unit +
+               pieces_max * tile_bytes / l2_per_unit_sm;
+    };
+    int Gsk = 1;
+    double sk = 1e300;
+    for (int chunk : {1, 2, 4, 8}) {
+        const int g = int(std::max<int64_t>(1, std::min<int64_t>(G, W / chunk)));
+        const double c = sk_cost(g);
+        if (c < sk * 0.99) {
+            sk = c;
+            Gsk = g;
+        }
+    }
     bool use_sk = sk < dp * 0.98;
     // AMSIM_SCHED=dp|sk forces a schedule (tests and tuning only; policy bit 1 still wins)
     if (const char *f = std::getenv("AMSIM_SCHED"); f && *f) use_sk = f[0] == 's';
