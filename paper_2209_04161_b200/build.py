@@ -70,9 +70,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
-def build_variant(tag: str, defines) -> str:
+def build_variant(tag: str, defines, only=None) -> str:
     """Experimental build with extra -D flags (tuning sweeps): build/variants/libamsim_<tag>.so.
-    Load it by setting AMSIM_LIB to the returned path."""
+    Load it by setting AMSIM_LIB to the returned path.  `only`: the translation
+    units to rebuild with the flags (the others are linked from the main build)."""
     vdir = os.path.join(BUILD, "variants")
     os.makedirs(vdir, exist_ok=True)
     host_o = os.path.join(BUILD, "amsim_host.cpp.o")
@@ -81,6 +82,9 @@ def build_variant(tag: str, defines) -> str:
     objs, procs = [host_o], []
     for src, tool in SOURCES:
         if tool != "nvcc":
+            continue
+        if only and src not in only:
+            objs.append(os.path.join(BUILD, src + ".o"))
             continue
         ko = os.path.join(vdir, f"{src}_{tag}.o")
         objs.append(ko)
@@ -98,6 +102,9 @@ def build_variant(tag: str, defines) -> str:
 
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[1] == "--variant":
-        print(build_variant(sys.argv[2], sys.argv[3:]))
+        # --variant TAG [-DFLAG ...] [+unit.cu ...]
+        args = sys.argv[3:]
+        print(build_variant(sys.argv[2], [a for a in args if not a.startswith("+")],
+                            [a[1:] for a in args if a.startswith("+")] or None))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -46,6 +46,9 @@ namespace dev {
 #ifndef AMSIM_PACK8
 #define AMSIM_PACK8 0
 #endif
+#ifndef AMSIM_PACK8A
+#define AMSIM_PACK8A 0   // 8-bit tables: pack only the warp-shared A side (alpha | offset)
+#endif
 #ifndef AMSIM_ROWPRED
 #define AMSIM_ROWPRED 0   // zero-row skipping: one predicate per row (lut_row_if16) instead of per lookup
                           // (fewer SASS instructions, but measured 0.7 % slower on the step: off)
@@ -627,60 +630,86 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
     }
 }
 
-// Decode one raw operand tile into (alpha, offset) arrays laid out [BK][rows];
-// tracks min / max exponent fields over nonzero elements.
-// PACK: one word per element, alpha (bits 31..23) | offset (bits 22..0; shared
-// memory table offsets are < 2^18), halving the inner loop's operand loads.
+// Decode of one raw operand tile into (alpha, offset) arrays laid out
+// [BK][rows], four elements per call (a "quad", one 16-byte shared load):
+//  * raw [BK][rows] (kcontig 0) and tap-blocked [rows >> cbl][BK][1 << cbl]
+//    (kcontig 3): 4 consecutive rows at one k -> one 16-byte store per array;
+//  * k-contiguous raw [rows][BK + RAW_PAD] (cp.async, kcontig 1) and TMA tiles
+//    [rows][BK] with the 64-byte swizzle (16-B chunk ^= address bits 8..7,
+//    kcontig 2): 4 consecutive k of one row -> 4 coalesced word stores (lanes
+//    take consecutive rows, so the 16-byte loads are conflict-free).
+// Quad q of the BK * ROWS / 4.  Tracks, over the nonzero exponent fields,
+// tmax = max(bits & 0x7F800000) and tmin = min((bits & 0x7F800000) - 1)
+// (zeros wrap to 0xFFFFFFFF and drop out of the min).
+// PACK: one word per element, alpha (bits 31..23) | offset (bits 22..0;
+// shared-memory table offsets are < 2^18), halving the inner loop's operand loads.
+struct DecArgs {
+    int shift;            // 23 - m
+    uint32_t mask;        // 2^m - 1
+    int off_shift;        // table offset = off_base + (index << off_shift)
+    uint32_t off_base;
+    bool ecast;           // exponent casting (reading C23) active: elo > 1 or ehi < 254
+    uint32_t elo, ehi;
+};
+
 template <int ROWS, bool RAW_ALPHA = false, bool PACK = false>
-__device__ __forceinline__ void decode_elem(const float *raw, int kcontig, int cbl, int e, uint32_t *al, uint32_t *off,
-                                            int shift, uint32_t mask, int off_shift, uint32_t off_base,
-                                            uint32_t &emin, uint32_t &emax, uint32_t elo, uint32_t ehi)
+__device__ __forceinline__ void decode_quad(const float *raw, int kcontig, int cbl, int q, uint32_t *al, uint32_t *off,
+                                            const DecArgs &da, uint32_t &tmin, uint32_t &tmax)
 {
-    {
-        {
-            const int kk = e / ROWS, i = e % ROWS;
-            float v;
-            if (kcontig == 2) {  // TMA tile [ROWS][BK] with the 64-byte swizzle: 16-B chunk ^= address bits 8..7
-                uint32_t a = smem_u32(raw) + uint32_t(i * BK + kk) * 4u;
-                v = lds_f32(a ^ (((a >> 7) & 3u) << 4));
-            } else if (kcontig == 3) {  // tap-blocked [ROWS >> cbl][BK][1 << cbl]
-                v = raw[(((i >> cbl) * BK + kk) << cbl) | (i & ((1 << cbl) - 1))];
-            } else {
-                v = kcontig ? raw[i * (BK + RAW_PAD) + kk] : raw[kk * ROWS + i];
-            }
-            uint32_t u = __float_as_uint(v);
-            uint32_t ex = (u >> 23) & 0xFFu;
-            if (ex != 0 && ex != 255 && (ex < elo || ex > ehi)) {  // exponent cast to (1, e, m), reading C23
-                u = (u & 0x80000000u) | (ex > ehi ? 0x7F800000u : 0u);
-                ex = (u >> 23) & 0xFFu;
-            }
-            const uint32_t o = off_base + (((u >> shift) & mask) << off_shift);
-            if constexpr (PACK) {
-                al[e] = (u & 0xFF800000u) | o;
-            } else {
-                al[e] = RAW_ALPHA ? u : (u & 0xFF800000u);
-                off[e] = o;
-            }
-            if (ex) {
-                emin = min(emin, ex);
-                emax = max(emax, ex);
-            }
+    static_assert(ROWS % 4 == 0, "tile rows must be a multiple of 4");
+    uint32_t u[4];
+    int e[4];
+    const bool rowq = kcontig == 0 || kcontig == 3;
+    if (rowq) {   // 4 consecutive rows at one k
+        const int kk = q / (ROWS / 4), i = (q % (ROWS / 4)) * 4;
+        const int src = kcontig == 0 ? kk * ROWS + i : (((i >> cbl) * BK + kk) << cbl) | (i & ((1 << cbl) - 1));
+        const uint4 v = *reinterpret_cast<const uint4 *>(raw + src);
+        u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
+#pragma unroll
+        for (int j = 0; j < 4; j++) e[j] = kk * ROWS + i + j;
+    } else {      // 4 consecutive k of one row
+        const int i = q % ROWS, k4 = (q / ROWS) * 4;
+        uint32_t a;
+        if (kcontig == 2) {
+            a = smem_u32(raw) + uint32_t(i * BK + k4) * 4u;
+            a ^= ((a >> 7) & 3u) << 4;
+        } else {
+            a = smem_u32(raw + i * (BK + RAW_PAD) + k4);
+        }
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+        u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
+#pragma unroll
+        for (int j = 0; j < 4; j++) e[j] = (k4 + j) * ROWS + i;
+    }
+    uint32_t A[4], O[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        uint32_t x = u[j];
+        if (da.ecast) {   // exponent cast to (1, e, m), reading C23
+            const uint32_t ex = (x >> 23) & 0xFFu;
+            if (ex != 0 && ex != 255 && (ex < da.elo || ex > da.ehi)) x = (x & 0x80000000u) | (ex > da.ehi ? 0x7F800000u : 0u);
+        }
+        const uint32_t o = da.off_base + (((x >> da.shift) & da.mask) << da.off_shift);
+        const uint32_t t = x & 0x7F800000u;
+        tmax = max(tmax, t);
+        tmin = min(tmin, t - 1u);
+        if constexpr (PACK) {
+            A[j] = (x & 0xFF800000u) | o;
+        } else {
+            A[j] = RAW_ALPHA ? x : (x & 0xFF800000u);
+            O[j] = o;
         }
     }
-}
-
-template <int NT, int ROWS, bool RAW_ALPHA = false, bool PACK = false>
-__device__ __forceinline__ void decode_operand(const float *raw, int kcontig, int cbl, uint32_t *al, uint32_t *off,
-                                               int shift, uint32_t mask, int off_shift, uint32_t off_base,
-                                               uint32_t &emin, uint32_t &emax, uint32_t elo, uint32_t ehi)
-{
-    constexpr int total = BK * ROWS;
+    if (rowq) {
+        *reinterpret_cast<uint4 *>(al + e[0]) = make_uint4(A[0], A[1], A[2], A[3]);
+        if constexpr (!PACK) *reinterpret_cast<uint4 *>(off + e[0]) = make_uint4(O[0], O[1], O[2], O[3]);
+    } else {
 #pragma unroll
-    for (int e0 = 0; e0 < total; e0 += NT) {
-        const int e = e0 + threadIdx.x;
-        if (total % NT == 0 || e < total)
-            decode_elem<ROWS, RAW_ALPHA, PACK>(raw, kcontig, cbl, e, al, off, shift, mask, off_shift, off_base, emin,
-                                               emax, elo, ehi);
+        for (int j = 0; j < 4; j++) {
+            al[e[j]] = A[j];
+            if constexpr (!PACK) off[e[j]] = O[j];
+        }
     }
 }
 
@@ -736,6 +765,9 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // issue-bound and loses more to the unpacking than it gains: measured
     // +5.7 % / -3.8 % on the ResNet-50 step)
     constexpr bool PK = AMSIM_PACK && MUL == MUL_LUT && !GL && (EB >= 16 || AMSIM_PACK8);
+    // A side packed (the warp-shared rows: broadcast loads); the B side keeps
+    // separate alpha / offset arrays unless PK
+    constexpr bool PKA = PK || (AMSIM_PACK8A && MUL == MUL_LUT && !GL && EB == 8);
     // Zero-row skipping (normal orientation, LSU-bound 16/32-bit shared tables):
     // a warp-shared A element with a zero exponent field (+-0, subnormal) has
     // alpha_a = +-0, so its products add +-0 to acc (never -0: it starts at +0)
@@ -790,6 +822,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     const uint32_t a_off_base = MUL == MUL_LUT ? lut_base : (MUL == MUL_DIRECT_EXACT ? 0x3F800000u : 0u);
     const uint32_t b_off_base = MUL == MUL_DIRECT_EXACT ? 0x3F800000u : 0u;
     const uint32_t elo = uint32_t(p.ecast_lo), ehi = uint32_t(p.ecast_hi);
+    const DecArgs dargs_a{shift, mask, a_off_shift, a_off_base, elo > 1u || ehi < 254u, elo, ehi};
+    const DecArgs dargs_b{shift, mask, b_off_shift, b_off_base, elo > 1u || ehi < 254u, elo, ehi};
     const float *dummy = reinterpret_cast<const float *>(p.lut);  // valid global address for 0-byte copies
 
     // Work units: (tile t, k-tile range [k0, k1)); see SubP for the schedule.
@@ -957,9 +991,9 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // exponent ranges are published before the one barrier per k-tile, so the
     // decode's shared-memory latency hides behind the lookups instead of
     // stalling the whole CTA between k-tiles.
-    static_assert((BK * BM) % NT == 0 && (BK * BN) % NT == 0, "decode work must split evenly over the threads");
-    constexpr int NEA = BK * BM / NT, NEB = BK * BN / NT;        // elements per thread and k-tile
-    constexpr int QA = (NEA + BK - 1) / BK, QB = (NEB + BK - 1) / BK; // ... per kk step of the fast loop
+    // quads (4 elements, decode_quad) per thread and k-tile; the last round may be partial
+    constexpr int TQA = BK * BM / 4, TQB = BK * BN / 4;
+    constexpr int NQA = (TQA + NT - 1) / NT, NQB = (TQB + NT - 1) / NT;
     // Interleaving pays for the transposed orientation's 16-row tiles (Big^T /
     // Flat^T / Huge^T: 1.5-3.5 % faster on dense operands, neutral on layer
     // inputs) and for the normal 16 x 8 tile on dense errors (dgrad, 1 %); it
@@ -969,34 +1003,44 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // lookups of k-tile g, before the barrier.
     constexpr bool DA = AMSIM_DA != 0 && MUL == MUL_LUT && TM == 16 &&
                         (TRN ? TN % 4 == 0 : (DGRAD && TN == 8));
+    static_assert(NQA + NQB <= BK || !DA, "decode-ahead: one quad per kk step");
     static_assert(!Cf::NP || PK, "narrow (NP) tile configurations need the packed operand words");
-    constexpr int DSTR = PK ? 1 : 2;   // decoded words per element (packed: alpha | offset)
+    constexpr int DSTR = PKA ? 1 : 2;   // decoded words per A element (packed: alpha | offset)
     auto dec_a = [&](int gg) { return dec + (gg & 1) * Cf::DEC; };
     auto raw_of = [&](int gg) { return raw + (gg % STAGES) * Cf::RAW_STAGE; };
     auto wait_raw = [&](int gg) { mbar_wait(smem_u32(&bars[gg % STAGES]), uint32_t((gg / STAGES) & 1)); };
-    auto dec_one_a = [&](int gg, int i, uint32_t &mn, uint32_t &mx) {
-        uint32_t *d = dec_a(gg);
-        decode_elem<BM, MUL == MUL_NATIVE, PK>(raw_of(gg), p.da.kcontig, p.da.cblk_log2, i * NT + tid, d, d + BK * BM,
-                                               shift, mask, a_off_shift, a_off_base, mn, mx, elo, ehi);
+    auto dec_quad_a = [&](int gg, int j, uint32_t &mn, uint32_t &mx) {
+        const int q = j * NT + tid;
+        if (TQA % NT == 0 || q < TQA) {
+            uint32_t *d = dec_a(gg);
+            decode_quad<BM, MUL == MUL_NATIVE, PKA>(raw_of(gg), p.da.kcontig, p.da.cblk_log2, q, d, d + BK * BM, dargs_a,
+                                                    mn, mx);
+        }
     };
-    auto dec_one_b = [&](int gg, int i, uint32_t &mn, uint32_t &mx) {
-        uint32_t *d = dec_a(gg) + DSTR * BK * BM;
-        decode_elem<BN, MUL == MUL_NATIVE, PK>(raw_of(gg) + Cf::RAW_A, p.db.kcontig, p.db.cblk_log2, i * NT + tid, d,
-                                               d + BK * BN, shift, mask, b_off_shift, b_off_base, mn, mx, elo, ehi);
+    auto dec_quad_b = [&](int gg, int j, uint32_t &mn, uint32_t &mx) {
+        const int q = j * NT + tid;
+        if (TQB % NT == 0 || q < TQB) {
+            uint32_t *d = dec_a(gg) + DSTR * BK * BM;
+            decode_quad<BN, MUL == MUL_NATIVE, PK>(raw_of(gg) + Cf::RAW_A, p.db.kcontig, p.db.cblk_log2, q, d, d + BK * BN,
+                                                   dargs_b, mn, mx);
+        }
     };
-    auto publish = [&](int gg, uint32_t amin, uint32_t amax, uint32_t bmin, uint32_t bmax) {
-        amin = __reduce_min_sync(0xffffffffu, amin);
-        amax = __reduce_max_sync(0xffffffffu, amax);
-        bmin = __reduce_min_sync(0xffffffffu, bmin);
-        bmax = __reduce_max_sync(0xffffffffu, bmax);
+    // per-warp exponent ranges of k-tile gg -> wflags[gg & 1][warp]: bytes
+    // (Amin, Amax, Bmin, Bmax) of the nonzero exponent fields (decode_quad's
+    // tmin / tmax encoding; empty: min 255, max 0)
+    auto publish = [&](int gg, uint32_t tamin, uint32_t tamax, uint32_t tbmin, uint32_t tbmax) {
+        const uint32_t amin = __reduce_min_sync(0xffffffffu, (min(tamin, 0x7F7FFFFFu) + 1u) >> 23);
+        const uint32_t amax = __reduce_max_sync(0xffffffffu, tamax >> 23);
+        const uint32_t bmin = __reduce_min_sync(0xffffffffu, (min(tbmin, 0x7F7FFFFFu) + 1u) >> 23);
+        const uint32_t bmax = __reduce_max_sync(0xffffffffu, tbmax >> 23);
         if (lane == 0) wflags[(gg & 1) * NWARPS + warp] = amin | (amax << 8) | (bmin << 16) | (bmax << 24);
     };
     auto decode_all = [&](int gg) {
-        uint32_t amin = 255, amax = 0, bmin = 255, bmax = 0;
+        uint32_t amin = 0xFFFFFFFFu, amax = 0, bmin = 0xFFFFFFFFu, bmax = 0;
 #pragma unroll
-        for (int i = 0; i < NEA; i++) dec_one_a(gg, i, amin, amax);
+        for (int j = 0; j < NQA; j++) dec_quad_a(gg, j, amin, amax);
 #pragma unroll
-        for (int i = 0; i < NEB; i++) dec_one_b(gg, i, bmin, bmax);
+        for (int j = 0; j < NQB; j++) dec_quad_b(gg, j, bmin, bmax);
         publish(gg, amin, amax, bmin, bmax);
     };
 
@@ -1031,15 +1075,13 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             }
             uint32_t *d = dec_a(g);
             uint32_t *a_al = d, *a_off = d + BK * BM, *b_al = d + DSTR * BK * BM, *b_off = b_al + BK * BN;
-            const uint32_t *wf = wflags + (g & 1) * NWARPS;
-            uint32_t lo = 0xFFFFFFFFu, hi = 0u;  // byte-wise mins (bytes 0, 2), maxs (bytes 1, 3)
-#pragma unroll
-            for (int w = 0; w < NWARPS; w++) {
-                uint32_t v = wf[w];
-                lo = __vminu4(lo, v | 0xFF00FF00u);
-                hi = __vmaxu4(hi, v & 0xFF00FF00u);
-            }
-            const int Amin = lo & 0xFF, Bmin = (lo >> 16) & 0xFF, Amax = (hi >> 8) & 0xFF, Bmax = hi >> 24;
+            // the CTA's exponent ranges: lane w < NWARPS reads warp w's word, one
+            // warp-wide reduction per field
+            const uint32_t fw = lane < NWARPS ? wflags[(g & 1) * NWARPS + lane] : 0x00FF00FFu;
+            const int Amin = int(__reduce_min_sync(0xffffffffu, fw & 0xFFu));
+            const int Amax = int(__reduce_max_sync(0xffffffffu, (fw >> 8) & 0xFFu));
+            const int Bmin = int(__reduce_min_sync(0xffffffffu, (fw >> 16) & 0xFFu));
+            const int Bmax = int(__reduce_max_sync(0xffffffffu, fw >> 24));
             // The fast path equals Alg. 2 bit-for-bit when alpha_a is finite
             // (ea <= 254), x = entry * 2^(eb-127) is finite (eb <= 253) and,
             // for every pair of nonzero operands, 1 <= Exp (ea + eb >= 128)
@@ -1048,7 +1090,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             const bool fast = p.policy == 0 && Amax <= 254 && Bmax <= 253 &&
                               (Amax == 0 || Bmax == 0 || (Amin + Bmin >= 128 && Amax + Bmax <= 380));
             if (has_next) wait_raw(g + 1);
-            uint32_t namin = 255, namax = 0, nbmin = 255, nbmax = 0;   // k-tile g+1's exponent ranges (fast path)
+            uint32_t namin = 0xFFFFFFFFu, namax = 0, nbmin = 0xFFFFFFFFu, nbmax = 0;   // k-tile g+1's exponent ranges (fast path)
 
             const uint32_t *A_al = a_al + Cf::wrow(warp), *A_off = a_off + Cf::wrow(warp);
             // lane columns: groups of 4 consecutive columns, group g at g * 128
@@ -1082,19 +1124,15 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
             } else if (fast) {
 #pragma unroll KK_UNROLL
                 for (int kk = 0; kk < BK; kk++) {
-                    if (DA && has_next) {   // decode-ahead slice of k-tile g+1
-#pragma unroll
-                        for (int q = 0; q < QA; q++)
-                            if (kk * QA + q < NEA) dec_one_a(g + 1, kk * QA + q, namin, namax);
-#pragma unroll
-                        for (int q = 0; q < QB; q++)
-                            if (kk * QB + q < NEB) dec_one_b(g + 1, kk * QB + q, nbmin, nbmax);
+                    if (DA && has_next) {   // decode-ahead slice of k-tile g+1: quad kk
+                        if (kk < NQA) dec_quad_a(g + 1, kk, namin, namax);
+                        else if (kk < NQA + NQB) dec_quad_b(g + 1, kk - NQA, nbmin, nbmax);
                     }
                     uint32_t aal[TM], aof[TM], bal[TN], bof[TN], mul[TN];
 #pragma unroll
                     for (int r = 0; r < TM; r += 4) {
                         uint4 v = *reinterpret_cast<const uint4 *>(A_al + kk * BM + r);
-                        if constexpr (PK) {
+                        if constexpr (PKA) {
                             aal[r] = v.x & AMASK; aal[r + 1] = v.y & AMASK; aal[r + 2] = v.z & AMASK; aal[r + 3] = v.w & AMASK;
                             aof[r] = v.x & OMASK; aof[r + 1] = v.y & OMASK; aof[r + 2] = v.z & OMASK; aof[r + 3] = v.w & OMASK;
                         } else {
@@ -1164,8 +1202,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                 for (int kk = 0; kk < BK; kk++) {
 #pragma unroll
                     for (int r = 0; r < TM; r++) {
-                        uint32_t aal = A_al[kk * BM + r], aof = PK ? (aal & OMASK) : A_off[kk * BM + r];
-                        if (PK) aal &= AMASK;
+                        uint32_t aal = A_al[kk * BM + r], aof = PKA ? (aal & OMASK) : A_off[kk * BM + r];
+                        if (PKA) aal &= AMASK;
                         uint32_t ea = (aal >> 23) & 0xFFu;
 #pragma unroll
                         for (int c = 0; c < TN; c++) {

@@ -93,6 +93,12 @@ using CfgMid = KCfg<AMSIM_NT_MID, AMSIM_TM_MID, 2>;      // N <= 64, M > 64
 using CfgBig = KCfg<AMSIM_NT_BIG, AMSIM_TM_BIG, AMSIM_TN_BIG>;  // N > 64, M > 64
 using CfgLean = KCfg<256, 8, 2>;                         // N <= 64, M <= 64; and tables too large for the others
 using CfgWide = KCfg<256, 8, 4>;                         // N > 64, M <= 64
+#ifndef AMSIM_SK_ALIGN_PCT
+#define AMSIM_SK_ALIGN_PCT 0   // stream-K CTA count aligned to the tile count when it costs <= this % of the SMs
+#endif
+#ifndef AMSIM_HUGE8
+#define AMSIM_HUGE8 1   // offer the 16 x 8 tile to 8-bit tables too
+#endif
 using CfgHuge = KCfg<256, 16, 8>;                        // N >= 256, 16/32-bit tables (fewer operand loads per lookup)
 using CfgFlat = KCfg<256, 16, 4, 2>;                     // 64 x 256: 64-row problems (64-channel layers, transposed)
                                                          // with Big's 16 x 4 register tile instead of Wide's 8 x 4
@@ -224,6 +230,20 @@ static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int polic
         if (c < sk * 0.99) {
             sk = c;
             Gsk = g;
+        }
+    }
+    // Few tiles, each split over several CTAs (wgrad: a handful of weight tiles,
+    // K = N * OH * OW): with G not a multiple of the tile count, the CTAs of
+    // different tiles start at different k offsets, so tiles that share an
+    // operand slice (the error / activation rows of the same pixels) read it
+    // hundreds of k-tiles apart and L2 cannot serve the second read.  A CTA
+    // count that is a multiple of the tile count aligns every tile's pieces in
+    // k, at the cost of up to AMSIM_SK_ALIGN_PCT % of the SMs.
+    if (p.nsub == 1 && p.ntiles > 1 && p.ntiles * 2 <= Gsk && Gsk % p.ntiles != 0) {
+        const int Ga = (Gsk / p.ntiles) * p.ntiles;
+        if ((Gsk - Ga) * 100 <= Gsk * AMSIM_SK_ALIGN_PCT) {
+            sk = sk * Gsk / Ga;
+            Gsk = Ga;
         }
     }
     bool use_sk = sk < dp * 0.98;
@@ -409,7 +429,7 @@ static amsim_status prepare(const amsim_lut *lut, KParams &p, const Problem &pr,
         int mmax = 0;
         for (int i = 0; i < pr.nsub; i++) mmax = std::max(mmax, pr.M[i]);
         if (mmax <= 64) cands.push_back(CfgId::Wide);
-        if (eb >= 16) cands.push_back(CfgId::Huge);
+        if (eb >= 16 || AMSIM_HUGE8) cands.push_back(CfgId::Huge);
         // one 160-row tile for 129..160 rows (Mid / Lean would pad 147 rows to 256 / 192)
         if (pr.nsub == 1 && pr.M[0] > 128 && pr.M[0] <= CfgTall::BM) cands.push_back(CfgId::Tall);
     } else {
@@ -565,7 +585,7 @@ static amsim_status launch_eb(const KParams &p, const OpA &a, const OpB &b, cuda
     case CfgId::Flat: return launch_cfg<CfgFlat, EB>(p, a, b, st);
     case CfgId::Tall: return launch_cfg<CfgTall, EB>(p, a, b, st);
     case CfgId::Huge:
-        if constexpr (EB >= 16) return launch_cfg<CfgHuge, EB>(p, a, b, st);
+        if constexpr (EB >= 16 || AMSIM_HUGE8) return launch_cfg<CfgHuge, EB>(p, a, b, st);
         else return set_error(AMSIM_ERR_UNSUPPORTED, "internal: Huge tiles need 16/32-bit tables");
     default: return launch_cfg<CfgBig, EB>(p, a, b, st);
     }
