@@ -63,14 +63,37 @@ namespace dev {
 // measured 2-3 % faster there, 1-2 % slower everywhere else, tools/ab_bench.py)
 #define AMSIM_DECODE_LATE 0
 #endif
+#ifndef AMSIM_SKIP_BRANCH
+// conv fwd / wgrad in the normal orientation: a zero warp-shared row (ReLU zero)
+// is skipped by a warp-uniform branch -- lookups, IMAD and FFMA -- instead of
+// predicating only its lookups (measured: ResNet-50 MBM step 729.0 -> 716.0 ms,
+// fwd -4.5 %, wgrad -0.9 %; Mitchell 600.6 -> 594.3 ms; profiles/r02b_ab_skipb_tree_*.jsonl)
+#define AMSIM_SKIP_BRANCH 1
+#endif
+#ifndef AMSIM_PACK_ACT
+#define AMSIM_PACK_ACT 1      // packed operand words also for the conv fwd / wgrad (layer-input) kernels
+                              // (0 measured 2.6 % slower on the step)
+#endif
+#ifndef AMSIM_SK_TREE
+#define AMSIM_SK_TREE 1   // stream-K pieces summed by a binary tree (0: by the last piece, serially)
+#endif
 #ifndef AMSIM_DA
-#define AMSIM_DA 1   // interleave the decode of k-tile g+1 with the fast-path lookups of k-tile g
+// interleave the decode of k-tile g+1 with the fast-path lookups of k-tile g
+// (1: the configurations where it measured faster with the round-2 per-element
+// decode; 2: every 16-row tile; 0: never -- since the quad decode the
+// un-interleaved order is 1 % faster on the ResNet-50 step, DA = 1 / 2 / 0:
+// 731.8 / 753.1 / 724.8 ms, profiles/r02b_ab_da_mbm.jsonl)
+#define AMSIM_DA 0
+#endif
+#ifndef AMSIM_LATE8
+#define AMSIM_LATE8 1   // 8-bit-table conv fwd / wgrad kernels decode each k-tile right before its lookups
 #endif
 
 constexpr int BK = 16;
 constexpr int STAGES = 3;
 constexpr int RAW_PAD = 4;    // row padding of k-contiguous raw tiles (keeps 16-B alignment)
 constexpr int MAX_SUB = 9;    // sub-problems per launch (stride phases of dgrad, S <= 3)
+constexpr int SK_LEVELS = 9;  // stream-K fix-up tree levels (<= 512 pieces per tile)
 
 // ---------------------------------------------------------------------------
 // PTX helpers
@@ -764,7 +787,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // shared memory (global table offsets can exceed 23 bits; the 8-bit path is
     // issue-bound and loses more to the unpacking than it gains: measured
     // +5.7 % / -3.8 % on the ResNet-50 step)
-    constexpr bool PK = AMSIM_PACK && MUL == MUL_LUT && !GL && (EB >= 16 || AMSIM_PACK8);
+    constexpr bool PK = AMSIM_PACK && MUL == MUL_LUT && !GL && (EB >= 16 || AMSIM_PACK8) &&
+                        (AMSIM_PACK_ACT || Cf::NP || !(is_act_op<OpA>::value || is_act_op<OpB>::value));
     // A side packed (the warp-shared rows: broadcast loads); the B side keeps
     // separate alpha / offset arrays unless PK
     constexpr bool PKA = PK || (AMSIM_PACK8A && MUL == MUL_LUT && !GL && EB == 8);
@@ -782,6 +806,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     constexpr bool DGRAD = is_dgrad_op<OpA>::value || is_dgrad_op<OpB>::value;
     constexpr bool SKIP = AMSIM_SKIP && MUL == MUL_LUT && !GL && EB >= 16 && !TRN && TN >= 4 && (!DGRAD || AMSIM_DGRAD_SKIP);
     constexpr bool ROWPRED = SKIP && AMSIM_ROWPRED && EB == 16 && (TN == 4 || TN == 8);
+    // branch-skipping of zero rows (layer-input A operands in the normal
+    // orientation: conv fwd / wgrad), also for 8-bit tables
+    constexpr bool SKIPB = AMSIM_SKIP_BRANCH && MUL == MUL_LUT && !GL && !TRN && TN >= 4 &&
+                           (is_act_op<OpA>::value || is_act_op<OpB>::value);
     constexpr uint32_t AMASK = 0xFF800000u, OMASK = 0x007FFFFFu;
     extern __shared__ __align__(128) unsigned char smem[];
 
@@ -1002,7 +1030,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // profiles/r02_cfg_da*.jsonl); elsewhere k-tile g+1 is decoded after the
     // lookups of k-tile g, before the barrier.
     constexpr bool DA = AMSIM_DA != 0 && MUL == MUL_LUT && TM == 16 &&
-                        (TRN ? TN % 4 == 0 : (DGRAD && TN == 8));
+                        (AMSIM_DA == 2 || (TRN ? TN % 4 == 0 : (DGRAD && TN == 8)));
     static_assert(NQA + NQB <= BK || !DA, "decode-ahead: one quad per kk step");
     static_assert(!Cf::NP || PK, "narrow (NP) tile configurations need the packed operand words");
     constexpr int DSTR = PKA ? 1 : 2;   // decoded words per A element (packed: alpha | offset)
@@ -1049,7 +1077,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 #pragma unroll
     for (int c = 0; c < TN; c++) ecur[c] = 0;
     int g = 0;
-    constexpr bool LATE = AMSIM_DECODE_LATE != 0 || (EB == 8 && MUL == MUL_LUT && (is_act_op<OpA>::value || is_act_op<OpB>::value));
+    constexpr bool LATE = AMSIM_DECODE_LATE != 0 ||
+                          (AMSIM_LATE8 && EB == 8 && MUL == MUL_LUT && (is_act_op<OpA>::value || is_act_op<OpB>::value));
     if (!LATE && ig > 0) {   // the CTA's first k-tile
         wait_raw(0);
         decode_all(0);
@@ -1174,6 +1203,19 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                     for (int c = 0; c < TN; c++) mul[c] = min(bal[c] << 1, MULV);
 #pragma unroll
                     for (int r = 0; r < TM; r++) {
+                        if constexpr (SKIPB) {
+                            // a zero warp-shared element: the whole row (lookups, IMAD,
+                            // FFMA) is skipped by a warp-uniform branch -- its products
+                            // are +-0 and acc + (+-0) = acc (acc is never -0)
+                            if ((aal[r] << 1) == 0u) continue;
+#pragma unroll
+                            for (int c = 0; c < TN; c++) {
+                                const uint32_t e = lut_entry<EB, GL>(aof[r] + bof[c], lut_g);
+                                const uint32_t x = e * mul[c] + bal[c];
+                                acc[r][c] = fma_ftz(__uint_as_float(x), __uint_as_float(aal[r]), acc[r][c]);
+                            }
+                            continue;
+                        }
                         if constexpr (ROWPRED) {
                             uint32_t ad[TN];
 #pragma unroll
@@ -1240,44 +1282,77 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
 
         const SubP &S = p.sub[T.s];
         if (T.partial) {
-            // Stream-K piece: store the partial sums (slot 2c for the CTA's first
-            // stream-K unit, 2c + 1 for its last; [TM * TN][NT] so every store
-            // and load is coalesced -- thread tid owns the same outputs of the
-            // tile in every CTA), publish, and let the piece that arrives last
-            // add all pieces in increasing k order (deterministic: the pieces and
-            // their order depend only on the plan) and write the tile.
+            // Stream-K piece: the tile's pieces (CTAs ca..cb, in k order) are
+            // summed by a binary tree fixed by the plan -- node (level l, n)
+            // adds the sums of pieces [n 2^l, n 2^l + 2^(l-1)) and
+            // [n 2^l + 2^(l-1), (n+1) 2^l) -- so the result is deterministic
+            // and nothing waits on another CTA: a CTA stores its subtree's sum
+            // in the subtree's leftmost slot ([TM * TN][NT], coalesced; slot 2c
+            // for CTA c's first stream-K unit, 2c + 1 for its last) and bumps
+            // the node's counter; the second arrival adds the two and climbs.
+            // The root's last arrival writes the tile.  (A single last-piece
+            // fix-up read all pieces serially: 74 pieces of 128 KB for a
+            // 2-tile wgrad at batch 32; the tree's critical path is
+            // ceil(log2 P) reads and writes.)
             const int P = CS.u.P, w = max(S.kt, 1);
             auto cta_of = [&](int pos) { return int((int64_t(pos + 1) * p.sk_G - 1) / p.sk_W); };
             auto lo_of = [&](int c) { return int(int64_t(c) * p.sk_W / p.sk_G); };
-            auto slot = [&](int c) {
-                return p.ws + (size_t(2 * c + (lo_of(c) < P ? 1 : 0)) * (TM * TN)) * NT + tid;
-            };
-            const int ca = cta_of(P), cb = cta_of(P + w - 1);
-            float *mine = slot(blockIdx.x);
+            auto pid = [&](int c) { return 2 * c + (lo_of(c) < P ? 1 : 0); };
+            auto slot = [&](int c) { return p.ws + size_t(pid(c)) * (TM * TN) * NT + tid; };
+            const int ca = cta_of(P), cb = cta_of(P + w - 1), np = cb - ca + 1, j = int(blockIdx.x) - ca;
+            unsigned *cnt = reinterpret_cast<unsigned *>(p.ws + size_t(2 * p.sk_G) * (TM * TN) * NT);
+            bool done = true;   // this CTA ends up holding the whole tile's sum
+            if constexpr (!AMSIM_SK_TREE) {
+                // round-2 first version: every piece stores its partial sums; the last
+                // to arrive (one counter per tile) reads all pieces in increasing k
+                float *mine = slot(blockIdx.x);
 #pragma unroll
-            for (int r = 0; r < TM; r++)
+                for (int r = 0; r < TM; r++)
 #pragma unroll
-                for (int c = 0; c < TN; c++) __stcg(mine + (r * TN + c) * NT, acc[r][c]);
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) {
-                unsigned *cnt = reinterpret_cast<unsigned *>(p.ws + size_t(2 * p.sk_G) * (TM * TN) * NT);
-                *sk_last = atomicAdd(cnt + (CS.u.t - p.n_dp), 1u) + 1 == unsigned(cb - ca + 1);
+                    for (int c = 0; c < TN; c++) __stcg(mine + (r * TN + c) * NT, acc[r][c]);
+                __threadfence();
+                __syncthreads();
+                if (tid == 0) *sk_last = atomicAdd(cnt + pid(ca), 1u) + 1 == unsigned(np);
+                __syncthreads();
+                if (!*sk_last) continue;
+                __threadfence();
+#pragma unroll
+                for (int r = 0; r < TM; r++)
+#pragma unroll
+                    for (int c = 0; c < TN; c++) acc[r][c] = 0.0f;
+                for (int q = ca; q <= cb; q++) {
+                    const float *src = slot(q);
+#pragma unroll
+                    for (int r = 0; r < TM; r++)
+#pragma unroll
+                        for (int c = 0; c < TN; c++) acc[r][c] += __ldcg(src + (r * TN + c) * NT);
+                }
             }
-            __syncthreads();
-            if (!*sk_last) continue;
-            __threadfence();
+            for (int l = 1; AMSIM_SK_TREE && (1 << (l - 1)) < np; l++) {
+                const int left = (j >> l) << l, right = left + (1 << (l - 1));
+                if (right >= np) continue;   // no right subtree: the sum passes through
+                const bool mine_left = j < right;
+                float *dst = slot(ca + (mine_left ? left : right));   // my subtree's leftmost slot
 #pragma unroll
-            for (int r = 0; r < TM; r++)
+                for (int r = 0; r < TM; r++)
 #pragma unroll
-                for (int c = 0; c < TN; c++) acc[r][c] = 0.0f;
-            for (int q = ca; q <= cb; q++) {
-                const float *src = slot(q);
+                    for (int c = 0; c < TN; c++) __stcg(dst + (r * TN + c) * NT, acc[r][c]);
+                __threadfence();
+                __syncthreads();
+                if (tid == 0) *sk_last = atomicAdd(cnt + (l - 1) * (2 * p.sk_G) + pid(ca + left), 1u) == 1u;
+                __syncthreads();
+                if (!*sk_last) {
+                    done = false;
+                    break;
+                }
+                __threadfence();
+                const float *src = slot(ca + (mine_left ? right : left));
 #pragma unroll
                 for (int r = 0; r < TM; r++)
 #pragma unroll
                     for (int c = 0; c < TN; c++) acc[r][c] += __ldcg(src + (r * TN + c) * NT);
             }
+            if (!done) continue;
         }
         // epilogue: this thread's TM x TN outputs
         if constexpr (TRN) {

@@ -208,8 +208,8 @@ static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int polic
     }
     const double dp = *std::max_element(load.begin(), load.end());
     // stream-K makespan: W / Gsk k-tiles, the per-unit overhead of the tiles a
-    // range touches, partial tiles through HBM, and the last piece's fix-up
-    // reading every piece of its tile
+    // range touches, partial tiles through HBM, and the fix-up tree's critical
+    // path (one partial tile written and one read per level, ceil(log2 pieces) levels)
     // small problems may use fewer CTAs than SMs (each at least `chunk` k-tiles):
     // the count that minimises the modelled time
     const double tile_bytes = 4.0 * BM * BN;
@@ -220,7 +220,7 @@ static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int polic
         for (int s = 0; s < pr.nsub; s++)
             pieces_max = std::max(pieces_max, std::ceil(std::max(p.sub[s].kt, 1) / per_cta) + 1.0);
         return std::ceil(per_cta) + tile_overhead * units + 2.0 * 2.0 * g * tile_bytes / hbm_per_unit +
-               pieces_max * tile_bytes / l2_per_unit_sm;
+               2.0 * std::ceil(std::log2(pieces_max)) * tile_bytes / l2_per_unit_sm;
     };
     int Gsk = 1;
     double sk = 1e300;
@@ -261,9 +261,9 @@ static double tile_plan(KParams &p, const Problem &pr, int BM, int BN, int polic
         pos += (tend - S.sk_tile) * std::max(S.kt, 1);
     }
     p.grid = std::max(p.n_dp > 0 ? std::min(p.n_dp, G) : 0, p.sk_G);
-    // workspace: 2 partial tiles per stream-K CTA, then one counter per stream-K tile
+    // workspace: 2 partial tiles per stream-K CTA, then the fix-up tree's counters
     p.ws = nullptr;
-    p.ws_elems = use_sk ? int64_t(2) * Gsk * BM * BN + (p.ntiles - p.n_dp) : 0;
+    p.ws_elems = use_sk ? int64_t(2) * Gsk * BM * BN + int64_t(SK_LEVELS) * 2 * Gsk : 0;
     (void)NT;
     return use_sk ? sk : dp;
 }
@@ -297,37 +297,37 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
 // Measured cost per padded approx-MAC (ns per G) of each tile configuration
 // with a 16-bit shared-memory table (MBM m = 7) under the stream-K schedule,
 // median over the ResNet-50 b256 passes of `tools/cfg_sweep.py`
-// (profiles/r02_cfg_sweep_b256.jsonl): dense operands (dgrad) and layer-input
+// (profiles/r02b_cfg_sweep_b256.jsonl, refit after the quad decode): dense operands (dgrad) and layer-input
 // A operands (fwd / wgrad: zero-row skipping in the normal orientation, sparse
 // lanes in the transposed one).  The wavefront model below under-prices the
 // instruction overhead of the smaller register tiles (Big 16x4 measures 1.13x
 // Huge 16x8 per MAC where the wavefronts predict 1.05x).  < 0: not measured.
 static double measured_cost16(CfgId c, bool trn, bool act)
 {
+    // refitted after the quad decode (profiles/r02b_cfg_sweep_b256.jsonl, tools/fit_costs.py)
     if (trn) {
         switch (c) {
-        case CfgId::Huge: return act ? 0.2562 : 0.2699;
-        case CfgId::Big: return act ? 0.2749 : 0.2870;
-        case CfgId::Flat: return act ? 0.2866 : 0.2990;
-        case CfgId::Flat3: return act ? 0.3071 : 0.3222;
-        case CfgId::Flat8: return act ? 0.2562 : 0.2699;   // not yet measured: Huge^T's (same 16 x 8 register tile)
-        case CfgId::TallT: return act ? 0.3068 : 0.3236;
-        case CfgId::Wide: return act ? 0.3153 : 0.3385;
+        case CfgId::Huge: return act ? 0.2387 : 0.2565;
+        case CfgId::Big: return act ? 0.2504 : 0.2686;
+        case CfgId::Flat: return act ? 0.2612 : 0.2809;
+        case CfgId::Flat3: return act ? 0.2701 : 0.2900;
+        case CfgId::Flat8: return act ? 0.2447 : 0.2597;
+        case CfgId::TallT: return act ? 0.2363 : 0.2305;
+        case CfgId::Wide: return act ? 0.2754 : 0.2959;
         default: return -1.0;
         }
     }
     switch (c) {
-    case CfgId::Huge: return act ? 0.2176 : 0.2689;
-    case CfgId::Big: return act ? 0.2652 : 0.3021;
-    case CfgId::Flat: return act ? 0.2702 : 0.3101;
-    case CfgId::Mid: return act ? 0.3399 : 0.3513;
-    case CfgId::Lean: return act ? 0.4039 : 0.4198;
-    case CfgId::Small: return act ? 0.5517 : 0.5769;
+    case CfgId::Huge: return act ? 0.1984 : 0.2523;
+    case CfgId::Big: return act ? 0.2407 : 0.2795;
+    case CfgId::Flat: return act ? 0.2481 : 0.2799;
+    case CfgId::Mid: return act ? 0.3006 : 0.3082;
+    case CfgId::Lean: return act ? 0.3486 : 0.3609;
+    case CfgId::Small: return act ? 0.4767 : 0.4927;
     // offered only for <= 64 (Wide) / 129..160 rows (Tall), absent from the sweep's
-    // shapes: Tall from the r01 stem-wgrad ratio to TallT^T (1.093), Wide between
-    // Big and Wide^T
-    case CfgId::Tall: return act ? 0.3410 : 0.3600;
-    case CfgId::Wide: return act ? 0.3000 : 0.3300;
+    // shapes: the round-2 guesses scaled by the sweep's mean change (x 0.91)
+    case CfgId::Tall: return act ? 0.3100 : 0.3280;
+    case CfgId::Wide: return act ? 0.2730 : 0.3000;
     default: return -1.0;
     }
 }
@@ -832,9 +832,10 @@ static amsim_status run(int eb, KParams p, const OpA &a, const OpB &b, cudaStrea
             own = true;
         }
         p.ws = ws;
-        // stream-K tile counters start at zero (one per stream-K tile, after the partial slots)
-        const int64_t slots = p.ws_elems - (p.ntiles - p.n_dp);
-        cudaError_t e = cudaMemsetAsync(ws + slots, 0, size_t(p.ntiles - p.n_dp) * 4, st);
+        // stream-K fix-up tree counters start at zero (SK_LEVELS x 2 per stream-K CTA,
+        // after the partial slots)
+        const int64_t ncnt = int64_t(SK_LEVELS) * 2 * p.sk_G;
+        cudaError_t e = cudaMemsetAsync(ws + (p.ws_elems - ncnt), 0, size_t(ncnt) * 4, st);
         if (e != cudaSuccess) {
             if (own) scratch_free(ws, st);
             return cuda_check(e, "stream-K counter reset");

@@ -1172,8 +1172,9 @@ def test_path_policy_is_per_thread(am, luts, orc):
 
 
 # ---------------------------------------------------------------------------
-# stream-K schedule (SubP in csrc/amsim_device.cuh): pieces of a tile summed
-# in increasing k by the last piece to finish
+# stream-K schedule (SubP in csrc/amsim_device.cuh): the pieces of a tile are
+# summed by a binary tree over their k order that depends only on the plan
+# (each node added by the second of its two subtrees to finish)
 
 SK_CASES = [
     # (kind, args): GEMM (M, N, K) or conv shape; chosen so tiles are cut into
