@@ -74,6 +74,14 @@ namespace dev {
 #define AMSIM_PACK_ACT 1      // packed operand words also for the conv fwd / wgrad (layer-input) kernels
                               // (0 measured 2.6 % slower on the step)
 #endif
+#ifndef AMSIM_ADDR_OR
+// table address = row offset | column offset (an ALU-pipe LOP3) instead of + (an
+// FMA-pipe IMAD.IADD): measured ResNet-50 MBM step 717.3 -> 707.0 ms, Mitchell
+// 594.3 -> 585.4 ms, 16384^3 Mitchell GEMM 5.64 -> 5.79 T/s (same box,
+// profiles/r02b_ab_addror_*.jsonl).  Round 1 measured it 3-6 % slower, when the
+// per-element decode kept the ALU pipe busy.
+#define AMSIM_ADDR_OR 1
+#endif
 #ifndef AMSIM_SK_TREE
 #define AMSIM_SK_TREE 1   // stream-K pieces summed by a binary tree (0: by the last piece, serially)
 #endif
@@ -808,9 +816,16 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     constexpr bool ROWPRED = SKIP && AMSIM_ROWPRED && EB == 16 && (TN == 4 || TN == 8);
     // branch-skipping of zero rows (layer-input A operands in the normal
     // orientation: conv fwd / wgrad), also for 8-bit tables
-    constexpr bool SKIPB = AMSIM_SKIP_BRANCH && MUL == MUL_LUT && !GL && !TRN && TN >= 4 &&
+    // (16 x 8 tiles only: with 4 columns per row the branch is not amortised --
+    // l2.x.conv2 wgrad on 16 x 4 tiles 7.10 -> 8.07 ms, profiles/r02b_cfg_sweep_b256*.jsonl)
+    constexpr bool SKIPB = AMSIM_SKIP_BRANCH && MUL == MUL_LUT && !GL && !TRN && TN >= 8 &&
                            (is_act_op<OpA>::value || is_act_op<OpB>::value);
     constexpr uint32_t AMASK = 0xFF800000u, OMASK = 0x007FFFFFu;
+    // table address = row offset + column offset; with AMSIM_ADDR_OR the two are
+    // OR-ed (an ALU-pipe LOP3 instead of an FMA-pipe IMAD.IADD): exact because the
+    // shared table is aligned to its row size (checked on the host) and the
+    // column offset is < the row size
+    auto ADDR = [](uint32_t ro, uint32_t co) { return (AMSIM_ADDR_OR && !GL) ? (ro | co) : (ro + co); };
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -842,6 +857,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     const uint32_t mask = (1u << m) - 1u;
     constexpr int ebytes_log2 = EB == 8 ? 0 : (EB == 16 ? 1 : 2);
     const uint32_t lut_base = GL ? 0u : smem_u32(lut_s);
+    // ADDR_OR needs the shared table aligned to its row size (<= 512 B for every
+    // shared-memory table); dynamic shared memory starts 1 KB-aligned on sm_100, and
+    // a violation fails loudly instead of reading wrong entries
+    if (AMSIM_ADDR_OR && !GL && MUL == MUL_LUT && (lut_base & ((1u << (m + ebytes_log2)) - 1u))) __trap();
     // entry << (32 - EB) restores the Alg. 1 layout (carry << 23) | mantissa
     constexpr uint32_t MULV = MUL != MUL_LUT ? 1u : (EB == 8 ? 65536u : (EB == 16 ? 256u : 1u));
     // decode: table byte offsets (LUT) or in-place truncated fractions (direct)
@@ -1206,11 +1225,13 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                         if constexpr (SKIPB) {
                             // a zero warp-shared element: the whole row (lookups, IMAD,
                             // FFMA) is skipped by a warp-uniform branch -- its products
-                            // are +-0 and acc + (+-0) = acc (acc is never -0)
+                            // are +-0 and acc + (+-0) = acc (acc is never -0).  (Measured
+                            // slower: a vote to mark the branch uniform, 717 -> 740 ms;
+                            // issuing row r+1's lookups before row r's math, -> 808 ms.)
                             if ((aal[r] << 1) == 0u) continue;
 #pragma unroll
                             for (int c = 0; c < TN; c++) {
-                                const uint32_t e = lut_entry<EB, GL>(aof[r] + bof[c], lut_g);
+                                const uint32_t e = lut_entry<EB, GL>(ADDR(aof[r], bof[c]), lut_g);
                                 const uint32_t x = e * mul[c] + bal[c];
                                 acc[r][c] = fma_ftz(__uint_as_float(x), __uint_as_float(aal[r]), acc[r][c]);
                             }
@@ -1228,10 +1249,10 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                             if constexpr (ROWPRED) {
                                 e = ecur[c];
                             } else if constexpr (SKIP) {
-                                lut_entry_if<EB>(ecur[c], aof[r] + bof[c], aal[r] << 1);
+                                lut_entry_if<EB>(ecur[c], ADDR(aof[r], bof[c]), aal[r] << 1);
                                 e = ecur[c];
                             } else {
-                                e = MUL == MUL_LUT ? lut_entry<EB, GL>(aof[r] + bof[c], lut_g)
+                                e = MUL == MUL_LUT ? lut_entry<EB, GL>(ADDR(aof[r], bof[c]), lut_g)
                                                    : direct_entry<MUL>(aof[r], bof[c]);
                             }
                             uint32_t x = e * mul[c] + bal[c];

@@ -160,12 +160,16 @@ static void finalize_lut(amsim_lut *lut)
     // 7 mantissa bits, e.g. Mitchell at m <= 7), 16 bits (carry | 15), else 32.
     uint32_t low = 0;
     for (uint32_t e : lut->entries) low |= e;
-    // The 8-bit layout only where it saves shared-memory wavefronts: a 2^m-entry
-    // row of 16-bit entries fits one 128-byte wavefront up to m = 6, and there
-    // LDS.U16 + the packed operand path measure 5.7 % faster than LDS.U8
-    // (4096^3 GEMM, Mitchell m = 4..6), so 8 bits is chosen from m = 7 on.
+    // Every table that fits 8 bits gets the 8-bit layout.  (Round 1 kept 16-bit
+    // entries up to m = 6, where a 2^m-entry 16-bit row still fits one 128-byte
+    // wavefront and LDS.U16 + packed operands measured 5.7 % faster; with the
+    // round-2 quad decode and 16 x 8 tiles for 8-bit tables the 8-bit layout is
+    // 19 % faster there: 4096^3 Mitchell m = 4..6, 4.92 -> 5.85 T/s,
+    // profiles/r02b_ab_min_m8.jsonl.)
     const bool fits8 = (low & 0xFFFFu) == 0, fits16 = (low & 0xFFu) == 0;
-    lut->device_entry_bits = (fits8 && lut->m >= 7) ? 8 : (fits16 ? 16 : 32);
+    int min_m8 = 1;   // AMSIM_MIN_M8: tuning experiments only
+    if (const char *f = std::getenv("AMSIM_MIN_M8"); f && *f) min_m8 = std::atoi(f);
+    lut->device_entry_bits = (fits8 && lut->m >= min_m8) ? 8 : (fits16 ? 16 : 32);
     // symmetric tables (model(a, b) == model(b, a) on every probe pair) may be used
     // transposed, which the skinny-N kernel orientation needs
     const size_t n = size_t(1) << lut->m;

@@ -358,8 +358,8 @@ def test_conv_vs_oracle(am, luts, orc, shape, which, model):
     assert_bits(got, res.c32, f"{which} {shape} vs c32")
 
 
-@pytest.mark.parametrize("model,m,width", [("mitchell", 7, 8), ("exact", 3, 16), ("mbm", 7, 16), ("exact", 6, 16),
-                                             ("mitchell", 8, 16)])
+@pytest.mark.parametrize("model,m,width", [("mitchell", 7, 8), ("exact", 3, 8), ("mbm", 7, 16), ("exact", 6, 16),
+                                             ("mitchell", 8, 16), ("mitchell", 5, 8), ("exact", 4, 16)])
 def test_entry_layout_never_changes_bits(am, luts, orc, model, m, width):
     """The narrow device layouts (8-bit: carry | 7 mantissa bits; 16-bit) give
     the same bits as the 32-bit Alg. 1 layout (policy bit 2), for GEMM and all
