@@ -297,35 +297,36 @@ static double wf_per_lookup(CfgId c, int eb, int mbits, bool table_in_smem)
 // Measured cost per padded approx-MAC (ns per G) of each tile configuration
 // with a 16-bit shared-memory table (MBM m = 7) under the stream-K schedule,
 // median over the ResNet-50 b256 passes of `tools/cfg_sweep.py`
-// (profiles/r02b_cfg_sweep_b256.jsonl, refit after the quad decode): dense operands (dgrad) and layer-input
+// (profiles/r02b_cfg_sweep_b256_final.jsonl, refit in round 2): dense operands (dgrad) and layer-input
 // A operands (fwd / wgrad: zero-row skipping in the normal orientation, sparse
 // lanes in the transposed one).  The wavefront model below under-prices the
 // instruction overhead of the smaller register tiles (Big 16x4 measures 1.13x
 // Huge 16x8 per MAC where the wavefronts predict 1.05x).  < 0: not measured.
 static double measured_cost16(CfgId c, bool trn, bool act)
 {
-    // refitted after the quad decode (profiles/r02b_cfg_sweep_b256.jsonl, tools/fit_costs.py)
+    // refitted after the quad decode, the zero-row branch skipping (16 x 8) and the
+    // OR table addresses (profiles/r02b_cfg_sweep_b256_final.jsonl, tools/fit_costs.py)
     if (trn) {
         switch (c) {
-        case CfgId::Huge: return act ? 0.2387 : 0.2565;
-        case CfgId::Big: return act ? 0.2504 : 0.2686;
-        case CfgId::Flat: return act ? 0.2612 : 0.2809;
-        case CfgId::Flat3: return act ? 0.2701 : 0.2900;
-        case CfgId::Flat8: return act ? 0.2447 : 0.2597;
-        case CfgId::TallT: return act ? 0.2363 : 0.2305;
-        case CfgId::Wide: return act ? 0.2754 : 0.2959;
+        case CfgId::Huge: return act ? 0.2352 : 0.2571;
+        case CfgId::Big: return act ? 0.2602 : 0.2770;
+        case CfgId::Flat: return act ? 0.2652 : 0.2825;
+        case CfgId::Flat3: return act ? 0.2758 : 0.2939;
+        case CfgId::Flat8: return act ? 0.2445 : 0.2626;
+        case CfgId::TallT: return act ? 0.2377 : 0.2375;
+        case CfgId::Wide: return act ? 0.2828 : 0.3045;
         default: return -1.0;
         }
     }
     switch (c) {
-    case CfgId::Huge: return act ? 0.1984 : 0.2523;
-    case CfgId::Big: return act ? 0.2407 : 0.2795;
-    case CfgId::Flat: return act ? 0.2481 : 0.2799;
-    case CfgId::Mid: return act ? 0.3006 : 0.3082;
-    case CfgId::Lean: return act ? 0.3486 : 0.3609;
-    case CfgId::Small: return act ? 0.4767 : 0.4927;
+    case CfgId::Huge: return act ? 0.1814 : 0.2551;
+    case CfgId::Big: return act ? 0.2427 : 0.2816;
+    case CfgId::Flat: return act ? 0.2437 : 0.2809;
+    case CfgId::Mid: return act ? 0.3079 : 0.3174;
+    case CfgId::Lean: return act ? 0.3641 : 0.3736;
+    case CfgId::Small: return act ? 0.4882 : 0.5227;
     // offered only for <= 64 (Wide) / 129..160 rows (Tall), absent from the sweep's
-    // shapes: the round-2 guesses scaled by the sweep's mean change (x 0.91)
+    // shapes: the round-2 guesses scaled by the sweeps' mean change (x 0.91)
     case CfgId::Tall: return act ? 0.3100 : 0.3280;
     case CfgId::Wide: return act ? 0.2730 : 0.3000;
     default: return -1.0;
