@@ -696,7 +696,7 @@ def main():
     # DRAM traffic of the dominant kernel kind per layer pass, from the committed
     # ncu launch list of this same command (profiles/; tools/summarize_launches.py)
     traffic, traffic_note = None, None
-    tpath = next((os.path.join(ROOT, "profiles", f) for f in ("r02b_traffic.json", "r02_traffic.json", "r01_traffic.json")
+    tpath = next((os.path.join(ROOT, "profiles", f) for f in ("r02c_traffic.json", "r02b_traffic.json", "r02_traffic.json", "r01_traffic.json")
                   if os.path.exists(os.path.join(ROOT, "profiles", f))), "")
     if args.workload == "resnet50" and os.path.exists(tpath):
         t = json.load(open(tpath)).get(dom_kind)

@@ -1227,7 +1227,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
                             // FFMA) is skipped by a warp-uniform branch -- its products
                             // are +-0 and acc + (+-0) = acc (acc is never -0).  (Measured
                             // slower: a vote to mark the branch uniform, 717 -> 740 ms;
-                            // issuing row r+1's lookups before row r's math, -> 808 ms.)
+                            // issuing row r+1's lookups before row r's math, -> 808 ms;
+                            // rows in pairs (both rows' lookups together), 699 -> 895 ms.)
                             if ((aal[r] << 1) == 0u) continue;
 #pragma unroll
                             for (int c = 0; c < TN; c++) {
