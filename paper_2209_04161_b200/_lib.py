@@ -253,6 +253,13 @@ def amsim_gemm(lut: Lut, A, B, C, trans_a: bool = False, trans_b: bool = False, 
     M = A.shape[1] if trans_a else A.shape[0]
     K = A.shape[0] if trans_a else A.shape[1]
     N = B.shape[0] if trans_b else B.shape[1]
+    KB = B.shape[1] if trans_b else B.shape[0]
+    if KB != K or tuple(C.shape) != (M, N):
+        raise ValueError(f"amsim_gemm: op(A) is {M}x{K}, op(B) {KB}x{N}, C {tuple(C.shape)}")
+    dev = _T().cuda.current_device()
+    for t, nm in ((A, "A"), (B, "B"), (C, "C")):
+        if t.is_cuda and t.device.index != dev:
+            raise ValueError(f"{nm} is on {t.device}, not the current device cuda:{dev}")
     lds = []
     for t, nm in ((A, "A"), (B, "B"), (C, "C")):
         if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):

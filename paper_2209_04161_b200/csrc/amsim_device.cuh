@@ -43,6 +43,9 @@ namespace dev {
 #ifndef AMSIM_KK_UNROLL_SMALL
 #define AMSIM_KK_UNROLL_SMALL 2   // fast-path k unroll for register tiles of <= 64 products
 #endif
+#ifndef AMSIM_KK_UNROLL_LARGE
+#define AMSIM_KK_UNROLL_LARGE 2   // fast-path k unroll for larger register tiles
+#endif
 #ifndef AMSIM_PACK8
 #define AMSIM_PACK8 0
 #endif
@@ -808,7 +811,7 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     // value, so x stays finite under the fast-path conditions.  Same bits.
     // Only for TN >= 4: the per-row predicate costs one LOP3 per row and k,
     // which 1- and 2-column tiles cannot amortise (LeNet-5: +17 % measured).
-    constexpr int KK_UNROLL = TM * TN <= 64 ? AMSIM_KK_UNROLL_SMALL : 2;
+    constexpr int KK_UNROLL = TM * TN <= 64 ? AMSIM_KK_UNROLL_SMALL : AMSIM_KK_UNROLL_LARGE;
     // dgrad's A operand is the layer error (dense): AMSIM_DGRAD_SKIP = 0 would
     // give its kernels the plain lookups (measured slower, so off)
     constexpr bool DGRAD = is_dgrad_op<OpA>::value || is_dgrad_op<OpB>::value;

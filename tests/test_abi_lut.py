@@ -225,3 +225,16 @@ def test_c_example_runs(built, tmp_path):
     import subprocess
     r = subprocess.run([_build_example(tmp_path)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "amsim_example: ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_binding_rejects_inconsistent_gemm_shapes(built):
+    """The binding checks what the C ABI cannot see from pointers: op(A)'s K
+    must match op(B)'s and C must be M x N (host-side, before any call)."""
+    import torch
+    lut = am.Lut.build("mitchell", 7)
+    with pytest.raises(ValueError, match="op\\(A\\)"):
+        am.amsim_gemm(lut, torch.zeros(2, 3), torch.zeros(4, 5), torch.zeros(2, 5))
+    with pytest.raises(ValueError, match="op\\(A\\)"):
+        am.amsim_gemm(lut, torch.zeros(2, 3), torch.zeros(3, 5), torch.zeros(2, 4))
+    with pytest.raises(ValueError, match="op\\(A\\)"):
+        am.amsim_gemm(lut, torch.zeros(3, 2), torch.zeros(3, 5), torch.zeros(3, 5), trans_a=True)
