@@ -44,7 +44,8 @@ namespace dev {
 #define AMSIM_KK_UNROLL_SMALL 2   // fast-path k unroll for register tiles of <= 64 products
 #endif
 #ifndef AMSIM_KK_UNROLL_LARGE
-#define AMSIM_KK_UNROLL_LARGE 2   // fast-path k unroll for larger register tiles
+#define AMSIM_KK_UNROLL_LARGE 2   // fast-path k unroll for larger register tiles (1 / 4: +0.6 % / +12 %
+                                  // on the step, profiles/r02c_ab_unroll_*.jsonl)
 #endif
 #ifndef AMSIM_PACK8
 #define AMSIM_PACK8 0
