@@ -1006,6 +1006,39 @@ def test_zero_row_skipping_bits(am, luts, orc, policy):
 
 
 @pytest.mark.parametrize("model", ["mbm", "mitchell"])
+@pytest.mark.parametrize("policy", [2, 0])
+def test_zero_row_branch_skipping_16x8(am, luts, orc, model, policy, monkeypatch):
+    """Conv fwd / wgrad on the normal-orientation 16 x 8 tile (AMSIM_FORCE_CFG=5),
+    where a zero warp-shared layer-input element skips its whole row (lookups,
+    IMAD, FFMA) by a uniform branch: inputs with +0, -0 and subnormal elements,
+    all-zero pixels and channels, for the 16-bit (MBM) and 8-bit (Mitchell)
+    layouts -- the oracle's c32 bits in exact order (policy bit 1), the C12
+    tolerance in the default (stream-K) plan."""
+    monkeypatch.setenv("AMSIM_FORCE_CFG", "5")
+    lut = luts(model)
+    g = inp.rng(260)
+    for k, shape in enumerate([(2, 13, 13, 32, 256, 3, 3, 1, 1), (3, 9, 9, 64, 300, 1, 1, 1, 0)]):
+        x, w, dy, OH, OW = _conv_tensors(shape, 261 + k)
+        x[g.random(x.shape) < 0.1] = -0.0
+        sub = g.random(x.shape) < 0.03
+        x[sub] = (g.integers(1, 1 << 23, int(sub.sum())).astype(np.uint32)).view(np.float32)
+        x[0, :3] = 0.0            # all-zero pixels (rows of the fwd A operand)
+        x[..., :5] = 0.0          # all-zero channels (rows of the wgrad A operand)
+        d, od = am.conv_desc(*shape), orc.conv_desc(*shape)
+        refs = {"fwd": orc.conv_fwd(od, x, w, model), "wgrad": orc.conv_bwd_filter(od, x, dy, model)}
+        am.amsim_set_path_policy(policy)
+        try:
+            outs = {which: _run_conv(am, lut, d, x, w, dy, which) for which in refs}
+        finally:
+            am.amsim_set_path_policy(0)
+        for which, ref in refs.items():
+            if policy & 2:
+                assert_bits(outs[which], ref.c32, f"{model} {shape} {which} (exact order)")
+            else:
+                assert_tol(outs[which], ref, f"{model} {shape} {which}")
+
+
+@pytest.mark.parametrize("model", ["mbm", "mitchell"])
 def test_tall_tiles_129_to_160_rows(am, luts, orc, model, monkeypatch):
     """Problems of 129..160 rows (the stem's wgrad: M = 7*7*3 = 147) may use
     the 160 x 64 Tall tiles (20 x 2 register tiles); forced (AMSIM_FORCE_CFG=7)
