@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace amsim {
 namespace dev {
@@ -635,6 +636,81 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
     static_assert(ROWS % 4 == 0, "tile rows must be a multiple of 4");
     const int tid = threadIdx.x;
     const int vl = d.vec_log2;
+    if constexpr (std::is_same<Op, FwdX>::value && ROWS % NT == 0) {
+        // conv fwd input with C % 4 != 0 (the RGB stem, LeNet): 4-byte gathers, one
+        // output pixel per thread -- its (n, oh, ow) decomposed once, the k-tile's
+        // (kh, kw, ci) stepped incrementally -- instead of two fast divisions and a
+        // 64-bit address per element (~100 SASS instructions each, ncu on the stem)
+        if (d.kcontig == 1 && vl == 0) {
+            const ConvGeom &g = op.g;
+            uint32_t kh = g.fSC.div(uint32_t(k0)), r2 = uint32_t(k0) - kh * uint32_t(g.S * g.C);
+            uint32_t kw0 = g.fC.div(r2), ci0 = r2 - kw0 * g.C;
+            for (int i = tid; i < ROWS; i += NT) {
+                const int m = mn0 + i;
+                const bool rowok = m < op.M;
+                const uint32_t mm = rowok ? uint32_t(m) : 0u;
+                const uint32_t n = g.fOHOW.div(mm), r = mm - n * uint32_t(g.OH * g.OW);
+                const uint32_t oh = g.fOW.div(r), ow = r - oh * g.OW;
+                const int ihb = int(oh) * g.sh - g.ph, iwb = int(ow) * g.sw - g.pw;
+                const float *xb = op.x + int64_t(n) * g.H * g.W * g.C;
+                int h = int(kh), w = int(kw0), c = int(ci0);
+                const uint32_t dst0 = smem_u32(raw + i * (BK + RAW_PAD));
+#pragma unroll
+                for (int kk = 0; kk < BK; kk++) {
+                    const int ih = ihb + h, iw = iwb + w;
+                    const bool ok = rowok && k0 + kk < kend && k0 + kk < op.Kd && unsigned(ih) < unsigned(g.H) &&
+                                    unsigned(iw) < unsigned(g.W);
+                    const float *src = ok ? xb + (ih * g.W + iw) * g.C + c : dummy;
+                    cp_async4(dst0 + kk * 4, src, ok);
+                    if (++c == g.C) {
+                        c = 0;
+                        if (++w == g.S) {
+                            w = 0;
+                            ++h;
+                        }
+                    }
+                }
+            }
+            return;
+        }
+    }
+    if constexpr (std::is_same<Op, WgX>::value) {
+        // wgrad input with C % 4 != 0 (the RGB stem): raw [BK][ROWS], one weight row
+        // (kh, kw, ci) per thread, decomposed once; the k-tile's output pixels
+        // (n, oh, ow) stepped incrementally (lanes take consecutive rows: the smem
+        // writes stay conflict-free)
+        if (d.kcontig == 0 && vl == 0) {
+            const ConvGeom &g = op.g;
+            const uint32_t kq = uint32_t(min(k0, max(op.Kd - 1, 0)));
+            const uint32_t n0 = g.fOHOW.div(kq), rq = kq - n0 * uint32_t(g.OH * g.OW);
+            const uint32_t oh0 = g.fOW.div(rq), ow0 = rq - oh0 * g.OW;
+            for (int i = tid; i < ROWS; i += NT) {
+                const int m = mn0 + i;
+                const bool rowok = m < op.M;
+                const uint32_t mm = rowok ? uint32_t(m) : 0u;
+                const uint32_t kh = g.fSC.div(mm), r2 = mm - kh * uint32_t(g.S * g.C);
+                const uint32_t kw = g.fC.div(r2), ci = r2 - kw * g.C;
+                int n = int(n0), oh = int(oh0), ow = int(ow0);
+                const float *xc = op.x + ci;
+#pragma unroll
+                for (int kk = 0; kk < BK; kk++) {
+                    const int ih = oh * g.sh - g.ph + int(kh), iw = ow * g.sw - g.pw + int(kw);
+                    const bool ok = rowok && k0 + kk < kend && k0 + kk < op.Kd && unsigned(ih) < unsigned(g.H) &&
+                                    unsigned(iw) < unsigned(g.W);
+                    const float *src = ok ? xc + ((int64_t(n) * g.H + ih) * g.W + iw) * g.C : dummy;
+                    cp_async4(smem_u32(raw + kk * ROWS + i), src, ok);
+                    if (++ow == g.OW) {
+                        ow = 0;
+                        if (++oh == g.OH) {
+                            oh = 0;
+                            ++n;
+                        }
+                    }
+                }
+            }
+            return;
+        }
+    }
     if (d.kcontig) {  // raw [ROWS][BK + RAW_PAD]
         const int cpr_log2 = 4 - vl;  // chunks per row, BK = 16
         const int total = ROWS << cpr_log2;
