@@ -636,7 +636,7 @@ __device__ __forceinline__ void issue_operand(const Op &op, const OpDesc &d, flo
     static_assert(ROWS % 4 == 0, "tile rows must be a multiple of 4");
     const int tid = threadIdx.x;
     const int vl = d.vec_log2;
-    if constexpr (std::is_same<Op, FwdX>::value && ROWS % NT == 0) {
+    if constexpr (std::is_same<Op, FwdX>::value) {
         // conv fwd input with C % 4 != 0 (the RGB stem, LeNet): 4-byte gathers, one
         // output pixel per thread -- its (n, oh, ow) decomposed once, the k-tile's
         // (kh, kw, ci) stepped incrementally -- instead of two fast divisions and a
