@@ -607,7 +607,8 @@ struct KCfg {
     static constexpr int DEC = (NP ? 1 : 2) * BK * (BM + BN);   // u32 per buffer (alpha + offset, or packed)
     static size_t smem_bytes(uint32_t lut_bytes)
     {
-        size_t lut = (lut_bytes + 127) & ~size_t(127);
+        // + 1 KB: room to align the shared table to 1 KB (OR-formed table addresses)
+        size_t lut = lut_bytes ? ((lut_bytes + 127) & ~size_t(127)) + 1024 : 0;
         return lut + sizeof(float) * RAW_STAGE * STAGES + sizeof(uint32_t) * DEC * 2 + sizeof(uint32_t) * NWARPS * 2 +
                8 * STAGES + 16 + 128;
     }
@@ -911,8 +912,11 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lut_pad = (GL || MUL != MUL_LUT) ? 0u : ((p.lut_bytes + 127u) & ~127u);
     const unsigned char *lut_g = reinterpret_cast<const unsigned char *>(p.lut);
-    unsigned char *lut_s = smem;
-    float *raw = reinterpret_cast<float *>(smem + lut_pad);
+    // the shared table starts 1 KB-aligned (dynamic shared memory already is on
+    // sm_100, so this offset is 0 in practice; smem_bytes reserves the room)
+    const uint32_t lut_align = lut_pad ? ((1024u - (smem_u32(smem) & 1023u)) & 1023u) : 0u;
+    unsigned char *lut_s = smem + lut_align;
+    float *raw = reinterpret_cast<float *>(smem + lut_align + lut_pad);
     uint32_t *dec = reinterpret_cast<uint32_t *>(raw + Cf::RAW_STAGE * STAGES);
     uint32_t *wflags = dec + Cf::DEC * 2;  // [2][NWARPS]
     uint64_t *bars = reinterpret_cast<uint64_t *>(wflags + NWARPS * 2);
@@ -938,8 +942,8 @@ __global__ void __launch_bounds__(Cf::NT, 1) amsim_mm_kernel(const __grid_consta
     constexpr int ebytes_log2 = EB == 8 ? 0 : (EB == 16 ? 1 : 2);
     const uint32_t lut_base = GL ? 0u : smem_u32(lut_s);
     // ADDR_OR needs the shared table aligned to its row size (<= 512 B for every
-    // shared-memory table); dynamic shared memory starts 1 KB-aligned on sm_100, and
-    // a violation fails loudly instead of reading wrong entries
+    // shared-memory table): lut_s is 1 KB-aligned above, and a violation would fail
+    // loudly instead of reading wrong entries
     if (AMSIM_ADDR_OR && !GL && MUL == MUL_LUT && (lut_base & ((1u << (m + ebytes_log2)) - 1u))) __trap();
     // entry << (32 - EB) restores the Alg. 1 layout (carry << 23) | mantissa
     constexpr uint32_t MULV = MUL != MUL_LUT ? 1u : (EB == 8 ? 65536u : (EB == 16 ? 256u : 1u));
